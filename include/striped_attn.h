@@ -1,0 +1,109 @@
+/* striped_attn.h -- C ABI of the B200 (sm_100a) striped / ring causal attention path.
+ *
+ * Drop-in boundary for the reference's hot path (ringsim, /root/reference/pkg/src/ringsim).
+ * The reference has no FFI: its seams are pure-Python functions.  Each entry point
+ * below names the reference function it replaces.  A ctypes binding of exactly these
+ * symbols is paper_2311_09431_b200/_lib.py; INTEGRATION.md shows the binding a
+ * ringsim maintainer would add.
+ *
+ * Conventions (all entry points):
+ *   - Caller-owned DEVICE buffers, plain pointers and element counts; the library never
+ *     allocates device memory and never throws across the ABI.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Return 0 = OK, >0 = invalid argument (nothing launched), <0 = CUDA error.
+ *     sa_last_error() returns a thread-local message for the last non-zero status.
+ *   - Thread-safe across distinct streams.
+ *   - Token-major layouts: Q/K/V/O/dO are bf16 [c, H, D] (row = token, heads
+ *     interleaved, D contiguous).  LSE / Dsum are fp32 [H, c].  Accumulators fp32.
+ *   - D (head dim) in {64, 128}; Hq % Hkv == 0 (grouped-query attention).
+ *   - softmax_scale multiplies QK^T (the reference's scale=True is 1/sqrt(D),
+ *     attention.py:137-138 / simulator.py:365).
+ */
+#ifndef STRIPED_ATTN_H_
+#define STRIPED_ATTN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* MaskKind, attention.py:42-46 (same order). */
+enum sa_mask_kind {
+  SA_MASK_FULLY_MASKED = 0,    /* no pair allowed: block skipped                    */
+  SA_MASK_FULLY_UNMASKED = 1,  /* every pair allowed                                */
+  SA_MASK_CAUSAL_INCLUSIVE = 2,/* allowed iff key row y <= query row x              */
+  SA_MASK_CAUSAL_EXCLUSIVE = 3 /* allowed iff y < x (striped, key stripe > q stripe) */
+};
+
+/* Scheme, layout.py:20-22. */
+enum sa_scheme { SA_SCHEME_CONTIGUOUS = 0, SA_SCHEME_STRIPED = 1 };
+
+/* Direction of sa_permute. */
+enum sa_direction { SA_PARTITION = 0, SA_GATHER = 1 };
+
+int sa_abi_version(void);
+const char* sa_last_error(void);
+/* Number of device kernels this library launched since load (for bench "gpu_launches"). */
+int64_t sa_launch_count(void);
+
+/* K1 -- stripe permute / unpermute of a row-major [n_seq, row_bytes] tensor.
+ * Replaces Layout.partition (layout.py:81-101) and Layout.gather (layout.py:103-117).
+ *   SA_PARTITION, device < 0 : dst = concat_d shard_d   (dst row d*c + x <- src row global_of(d, x))
+ *   SA_PARTITION, device = d : dst = shard_d only       ([c, row_bytes])
+ *   SA_GATHER,    device < 0 : dst[global_of(d, x)] <- src[d*c + x]   (exact inverse)
+ *   SA_GATHER,    device = d : scatter shard d (src [c, row]) into its rows of dst [n_seq, row]
+ * global_of: striped d + x*N, contiguous d*c + x (layout.py:62-70).  Bit-exact byte copy;
+ * works for any payload (Q/K/V rows, int64 position ids, ...).  row_bytes % 4 == 0. */
+int sa_permute(const void* src, void* dst, int64_t n_seq, int32_t n_dev, int64_t row_bytes,
+               int32_t scheme, int32_t direction, int32_t device, void* stream);
+
+/* K2+K3 -- one ring step of the forward for one rank (one query stripe vs the held
+ * key/value stripe), all heads.  Replaces _process_round (simulator.py:144-186) ->
+ * classify_tiles / accumulate_tile / _fold (attention.py:213-225, 296-328) and, on the last
+ * step, finalize (attention.py:331-336) plus the implied LSE = m + ln l.
+ *   q [c, hq, d], k/v [c, hkv, d] bf16.
+ *   o_acc [c, hq, d] fp32, lse [hq, c] fp32: running (normalised) output and LSE of the ring
+ *     steps so far; merged in place with this block's result (-inf safe).  first_step: the
+ *     previous state is ignored (o_acc may be NULL when first_step && last_step).
+ *   out [c, hq, d] bf16: written when last_step (may be NULL otherwise).
+ *   mask_kind: sa_mask_kind for (query stripe j, key stripe k), chosen by the host with
+ *     get_mask_striped / get_mask_ring (attention.py:155-183).  Tiles of 128x128 are
+ *     classified in-kernel with the reference rule (attention.py:194-210); SKIP tiles are
+ *     never computed.  Rows with no allowed key (strict mask, local row 0) leave the state
+ *     unchanged.  tiles_computed (nullable, device int64[1]) is incremented by the number
+ *     of 128x128 tiles computed per head (the reference's RoundStats counters). */
+int sa_fwd_block(const void* q, const void* k, const void* v, float* o_acc, float* lse, void* out,
+                 int64_t c, int32_t hq, int32_t hkv, int32_t d, float softmax_scale,
+                 int32_t mask_kind, int32_t first_step, int32_t last_step,
+                 int64_t* tiles_computed, void* stream);
+
+/* K4 -- backward preprocess: dsum[h, x] = sum_d dout[x,h,d] * out[x,h,d]; zeroes dq_acc.
+ * (No reference counterpart: ringsim has no backward.) */
+int sa_bwd_preprocess(const void* out, const void* dout, float* dsum, float* dq_acc, int64_t c,
+                      int32_t hq, int32_t d, void* stream);
+
+/* K5 -- one ring step of the backward for one rank (no reference counterpart).
+ * Recomputes P = exp(scale*QK^T - lse) under mask_kind with the GLOBAL lse, then
+ *   dq_acc [c,hq,d] fp32 += scale * dS K          (this rank's queries)
+ *   dk_acc [c,hkv,d] fp32 += scale * dS^T Q       (the held key stripe; travels with K)
+ *   dv_acc [c,hkv,d] fp32 += P^T dO               (travels with V)
+ * with dS = P o (dO V^T - dsum).  Same tile classification / skipping as sa_fwd_block. */
+int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, const float* lse,
+                 const float* dsum, float* dq_acc, float* dk_acc, float* dv_acc, int64_t c,
+                 int32_t hq, int32_t hkv, int32_t d, float softmax_scale, int32_t mask_kind,
+                 void* stream);
+
+/* dst_bf16[i] = bf16(src[i]) (finalises dq/dk/dv accumulators and skipped last steps). */
+int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
+
+/* Test-only: exercises the tcgen05 / TMA operand layouts the kernels rely on, on one
+ * 128x128x128 tile: s = a b^T, o = bf16(s) v, y = b^T v (a, b, v bf16 [128,128] row-major;
+ * outputs fp32 [128,128]). */
+int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* o, float* y,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STRIPED_ATTN_H_ */

@@ -1,0 +1,169 @@
+// C ABI entry points (include/striped_attn.h): argument validation + dispatch.
+#include "../../include/striped_attn.h"
+#include "internal.h"
+
+#include <atomic>
+#include <cstdio>
+#include <cudaTypedefs.h>
+#include <mutex>
+
+namespace sa {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& m) { g_err = m; }
+int fail_arg(const std::string& m) {
+  g_err = m;
+  return 1;
+}
+void count_launch(int n) { g_launches += n; }
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return -static_cast<int>(e);
+  }
+  count_launch();
+  return 0;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int32_t heads, int32_t dim,
+                   int32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail_arg("cuTensorMapEncodeTiled unavailable");
+  cuuint64_t sizes[3] = {(cuuint64_t)dim, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)dim * 2, (cuuint64_t)heads * dim * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), sizes,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[128];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return fail_arg(buf);
+  }
+  return 0;
+}
+
+int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail_arg("cuTensorMapEncodeTiled unavailable");
+  cuuint64_t sizes[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), sizes,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : fail_arg("cuTensorMapEncodeTiled(2d) failed");
+}
+
+static int check_heads(int64_t c, int32_t hq, int32_t hkv, int32_t d) {
+  if (c < 1) return fail_arg("block length c must be >= 1");
+  if (c > (int64_t(1) << 31) - 256) return fail_arg("block length too large");
+  if (hq < 1 || hkv < 1 || hq % hkv) return fail_arg("need hq >= 1, hkv >= 1, hq % hkv == 0");
+  if (d != 64 && d != 128) return fail_arg("head dim must be 64 or 128");
+  return 0;
+}
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace sa
+
+using namespace sa;
+
+extern "C" {
+
+int sa_abi_version(void) { return 1; }
+const char* sa_last_error(void) { return g_err.c_str(); }
+int64_t sa_launch_count(void) { return g_launches.load(); }
+
+int sa_permute(const void* src, void* dst, int64_t n_seq, int32_t n_dev, int64_t row_bytes,
+               int32_t scheme, int32_t direction, int32_t device, void* stream) {
+  if (!src || !dst) return fail_arg("null pointer");
+  if (n_dev < 1 || n_seq < n_dev || n_seq % n_dev)
+    return fail_arg("n_dev must evenly divide n_seq");  // layout.py:50-56
+  if (row_bytes <= 0 || row_bytes % 4) return fail_arg("row_bytes must be a positive multiple of 4");
+  if (scheme != SA_SCHEME_CONTIGUOUS && scheme != SA_SCHEME_STRIPED) return fail_arg("bad scheme");
+  if (direction != SA_PARTITION && direction != SA_GATHER) return fail_arg("bad direction");
+  if (device >= n_dev) return fail_arg("device out of range");
+  return launch_permute(src, dst, n_seq, n_dev, row_bytes, scheme, direction, device,
+                        static_cast<cudaStream_t>(stream));
+}
+
+int sa_fwd_block(const void* q, const void* k, const void* v, float* o_acc, float* lse, void* out,
+                 int64_t c, int32_t hq, int32_t hkv, int32_t d, float softmax_scale,
+                 int32_t mask_kind, int32_t first_step, int32_t last_step,
+                 int64_t* tiles_computed, void* stream) {
+  if (int r = check_heads(c, hq, hkv, d)) return r;
+  if (!q || !k || !v || !lse) return fail_arg("null q/k/v/lse");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v)) return fail_arg("q/k/v must be 16B aligned");
+  if (!(first_step && last_step) && !o_acc) return fail_arg("o_acc required across ring steps");
+  if (last_step && !out) return fail_arg("out required on the last step");
+  if (mask_kind < 0 || mask_kind > 3) return fail_arg("bad mask kind");
+  if (!(softmax_scale > 0.f)) return fail_arg("softmax_scale must be > 0");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (mask_kind == SA_MASK_FULLY_MASKED) {
+    // Nothing to fold (attention.py:198: SKIP).  Keep the state well defined.
+    if (first_step) {
+      if (last_step) return fail_arg("a single fully-masked step leaves every row dead");
+      if (int r = launch_fill_state(o_acc, lse, c, hq, d, st)) return r;
+    }
+    if (last_step) return launch_cast(o_acc, out, c * hq * d, st);
+    return 0;
+  }
+  return launch_fwd(q, k, v, o_acc, lse, out, c, hq, hkv, d, softmax_scale, mask_kind, first_step,
+                    last_step, tiles_computed, st);
+}
+
+int sa_bwd_preprocess(const void* out, const void* dout, float* dsum, float* dq_acc, int64_t c,
+                      int32_t hq, int32_t d, void* stream) {
+  if (int r = check_heads(c, hq, hq, d)) return r;
+  if (!out || !dout || !dsum || !dq_acc) return fail_arg("null pointer");
+  return launch_bwd_pre(out, dout, dsum, dq_acc, c, hq, d, static_cast<cudaStream_t>(stream));
+}
+
+int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, const float* lse,
+                 const float* dsum, float* dq_acc, float* dk_acc, float* dv_acc, int64_t c,
+                 int32_t hq, int32_t hkv, int32_t d, float softmax_scale, int32_t mask_kind,
+                 void* stream) {
+  if (int r = check_heads(c, hq, hkv, d)) return r;
+  if (!q || !k || !v || !dout || !lse || !dsum || !dq_acc || !dk_acc || !dv_acc)
+    return fail_arg("null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout))
+    return fail_arg("q/k/v/dout must be 16B aligned");
+  if (mask_kind < 0 || mask_kind > 3) return fail_arg("bad mask kind");
+  if (!(softmax_scale > 0.f)) return fail_arg("softmax_scale must be > 0");
+  if (mask_kind == SA_MASK_FULLY_MASKED) return 0;
+  return launch_bwd(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, c, hq, hkv, d,
+                    softmax_scale, mask_kind, static_cast<cudaStream_t>(stream));
+}
+
+int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream) {
+  if (!src || !dst || n < 0) return fail_arg("bad cast arguments");
+  if (n == 0) return 0;
+  return launch_cast(src, dst, n, static_cast<cudaStream_t>(stream));
+}
+
+int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* o, float* y,
+                  void* stream) {
+  if (!a || !b || !v || !s || !o || !y) return fail_arg("null pointer");
+  return launch_probe(a, b, v, s, o, y, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

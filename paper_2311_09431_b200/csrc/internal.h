@@ -1,0 +1,37 @@
+// Host-side internals shared by the .cu translation units (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+namespace sa {
+
+void set_error(const std::string& msg);
+int fail_arg(const std::string& msg);             // returns 1
+int check_launch(const char* what);               // 0 or -(cudaError)
+void count_launch(int n = 1);
+
+// 3-D tensor map over a token-major bf16 tensor [rows, heads, dim] with a
+// (64 x 1 x box_rows) box and 128-byte swizzle (one smem "panel" per box).
+int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int32_t heads, int32_t dim,
+                   int32_t box_rows);
+// 2-D bf16 [rows, cols] map, box (64 x box_rows), SW128 (probe kernel).
+int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int32_t box_rows);
+
+int launch_permute(const void* src, void* dst, int64_t n_seq, int32_t n_dev, int64_t row_bytes,
+                   int32_t scheme, int32_t direction, int32_t device, cudaStream_t st);
+int launch_probe(const void* a, const void* b, const void* v, float* s, float* o, float* y,
+                 cudaStream_t st);
+int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float* lse, void* out,
+               int64_t c, int32_t hq, int32_t hkv, int32_t d, float scale, int32_t kind,
+               int32_t first, int32_t last, int64_t* tiles, cudaStream_t st);
+int launch_bwd_pre(const void* out, const void* dout, float* dsum, float* dq_acc, int64_t c,
+                   int32_t hq, int32_t d, cudaStream_t st);
+int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse,
+               const float* dsum, float* dq, float* dk, float* dv, int64_t c, int32_t hq,
+               int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st);
+int launch_cast(const float* src, void* dst, int64_t n, cudaStream_t st);
+int launch_fill_state(float* o_acc, float* lse, int64_t c, int32_t hq, int32_t d, cudaStream_t st);
+
+}  // namespace sa
