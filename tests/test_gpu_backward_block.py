@@ -1,0 +1,85 @@
+"""GPU parity of the backward kernels (K4 preprocess + K5 block) against the builder's
+fp64 restatement (oracle.ringref.block_backward -- NOT REFERENCE, ringsim has no backward).
+
+Both sides get the same bf16 q/k/v/dO and the same (oracle) out / lse, so only the
+backward kernel is under test.  Bar: max-abs 2e-2 and rel-L2 1e-2 on the fp32
+accumulators (north star tolerance), dsum 1e-3."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ringref as R
+
+pytestmark = pytest.mark.gpu
+
+MAX_ABS, REL_L2 = 2e-2, 1e-2
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2311_09431_b200 import ops as _ops
+    return _ops
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-30))
+
+
+def oracle_fwd_block(q, k, v, kind, scale):
+    c = q.shape[0]
+    st = R.Accum.fresh(c, q.shape[1], v.shape[2])
+    R.process_block(st, q * scale, k, v, kind, c, c)
+    return R.finalize(st, allow_dead=True)
+
+
+@pytest.mark.parametrize("kind", [2, 3, 1])
+@pytest.mark.parametrize("c,hq,hkv,d", [(128, 1, 1, 128), (256, 2, 2, 128), (384, 4, 2, 64),
+                                         (1000, 2, 2, 128), (100, 1, 1, 64), (1024, 4, 1, 128),
+                                         (300, 2, 2, 64)])
+def test_block_backward_matches_restatement(ops, kind, c, hq, hkv, d):
+    gen = torch.Generator(device="cuda").manual_seed(c + 31 * hq + d + kind)
+    q = torch.randn(c, hq, d, device="cuda", generator=gen).bfloat16()
+    k = torch.randn(c, hkv, d, device="cuda", generator=gen).bfloat16()
+    v = torch.randn(c, hkv, d, device="cuda", generator=gen).bfloat16()
+    do = torch.randn(c, hq, d, device="cuda", generator=gen).bfloat16()
+    scale = 1.0 / math.sqrt(d)
+    qn, kn, vn, don = (t.float().cpu().numpy().astype(np.float64) for t in (q, k, v, do))
+    o_ref, lse_ref = oracle_fwd_block(qn, kn, vn, kind, scale)
+    out = torch.tensor(o_ref, device="cuda").bfloat16()
+    outn = out.float().cpu().numpy().astype(np.float64)
+    lse = torch.tensor(lse_ref, device="cuda", dtype=torch.float32).contiguous()
+    dsum = torch.empty(hq, c, device="cuda")
+    dq = torch.full((c, hq, d), 7.0, device="cuda")  # preprocess must zero it
+    dk = torch.zeros(c, hkv, d, device="cuda")
+    dv = torch.zeros(c, hkv, d, device="cuda")
+    ops.bwd_preprocess(out, do, dsum, dq)
+    ops.bwd_block(q, k, v, do, lse, dsum, dq, dk, dv, scale, kind)
+    torch.cuda.synchronize()
+    dsum_ref = np.einsum("shd,shd->hs", don, outn)
+    assert np.max(np.abs(dsum.cpu().numpy() - dsum_ref)) <= 1e-3
+    want = R.block_backward(qn, kn, vn, don, lse_ref.astype(np.float32).astype(np.float64),
+                            dsum_ref, kind, scale)
+    for name, got, w in (("dq", dq, want[0]), ("dk", dk, want[1]), ("dv", dv, want[2])):
+        g = got.cpu().numpy()
+        assert np.isfinite(g).all(), name
+        assert np.max(np.abs(g - w)) <= MAX_ABS, (name, np.max(np.abs(g - w)))
+        assert rel_l2(g, w) <= REL_L2, (name, rel_l2(g, w))
+
+
+def test_backward_accumulates_into_travelling_buffers(ops):
+    """dk/dv are += (they ride the ring); dq_acc is += across launches."""
+    c, h, d = 256, 2, 128
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v, do = (torch.randn(c, h, d, device="cuda", generator=gen).bfloat16() for _ in range(4))
+    lse = torch.randn(h, c, device="cuda").abs() + 5.0
+    dsum = torch.randn(h, c, device="cuda")
+    bufs = [torch.zeros(c, h, d, device="cuda") for _ in range(3)]
+    ops.bwd_block(q, k, v, do, lse, dsum, *bufs, 0.1, 2)
+    once = [b.clone() for b in bufs]
+    ops.bwd_block(q, k, v, do, lse, dsum, *bufs, 0.1, 2)
+    torch.cuda.synchronize()
+    for a, b in zip(once, bufs):
+        assert torch.allclose(2 * a, b, rtol=1e-5, atol=1e-5)
