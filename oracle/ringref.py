@@ -508,3 +508,43 @@ def useful_flops_fwd_bwd(n_seq: int, hq: int, d: int) -> float:
 
 def useful_flops_fwd(n_seq: int, hq: int, d: int) -> float:
     return 2.0 * d * hq * n_seq * (n_seq + 1)
+
+
+def tiled_causal_backward(q, k, v, do, o, lse, softmax_scale: float, tile: int = 512,
+                          dtype=np.float32):
+    """NOT REFERENCE.  Flash-style tiled causal backward for one head ([S, D] arrays),
+    O(S * tile) memory: the CPU counterpart of the GPU kernel used only as the
+    ``bench.py`` CPU baseline (the reference has no backward).  lse is [S]."""
+    q, k, v, do, o = (np.asarray(x, dtype=dtype) for x in (q, k, v, do, o))
+    lse = np.asarray(lse, dtype=dtype)
+    n = q.shape[0]
+    dsum = (do * o).sum(axis=1)
+    dq = np.zeros_like(q)
+    dk = np.zeros_like(k)
+    dv = np.zeros_like(v)
+    sc = dtype(softmax_scale)
+    for c0 in range(0, n, tile):
+        c1 = min(n, c0 + tile)
+        kt, vt = k[c0:c1], v[c0:c1]
+        for r0 in range(c0 - c0 % tile, n, tile):
+            r1 = min(n, r0 + tile)
+            s = (q[r0:r1] @ kt.T) * sc
+            p = np.exp(s - lse[r0:r1, None])
+            if r0 < c1:  # diagonal tile: y <= x
+                p[np.arange(c0, c1)[None, :] > np.arange(r0, r1)[:, None]] = 0
+            dv[c0:c1] += p.T @ do[r0:r1]
+            ds = p * (do[r0:r1] @ vt.T - dsum[r0:r1, None])
+            dq[r0:r1] += sc * (ds @ kt)
+            dk[c0:c1] += sc * (ds.T @ q[r0:r1])
+    return dq, dk, dv
+
+
+def tiled_causal_forward(q, k, v, softmax_scale: float, tile: int = 512, dtype=np.float32):
+    """The reference's streaming-softmax forward (attention.py:296-328 via
+    simulator.py:144-186) for one head, causal, row-major tiles.  Returns (o, lse)."""
+    q, k, v = (np.asarray(x, dtype=dtype) for x in (q, k, v))
+    st = Accum.fresh(q.shape[0], 1, v.shape[1], dtype)
+    process_block(st, (q * dtype(softmax_scale))[:, None], k[:, None], v[:, None],
+                  CAUSAL_INCLUSIVE, tile, tile)
+    o, lse = finalize(st)
+    return o[:, 0], lse[0]
