@@ -61,6 +61,20 @@ int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int32_t hea
   return 0;
 }
 
+int make_tmap_rows_f32(CUtensorMap* map, const void* base, int64_t rows, int32_t heads,
+                       int32_t dim, int32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail_arg("cuTensorMapEncodeTiled unavailable");
+  cuuint64_t sizes[3] = {(cuuint64_t)dim, (cuuint64_t)heads, (cuuint64_t)rows};
+  cuuint64_t strides[2] = {(cuuint64_t)dim * 4, (cuuint64_t)heads * dim * 4};
+  cuuint32_t box[3] = {32, 1, (cuuint32_t)box_rows};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), sizes, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : fail_arg("cuTensorMapEncodeTiled(f32) failed");
+}
+
 int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int32_t box_rows) {
   auto fn = encode_fn();
   if (!fn) return fail_arg("cuTensorMapEncodeTiled unavailable");

@@ -2,51 +2,62 @@
 // backward).  Same block mask, tile classification and skipping as the forward
 // (attention.py:155-183, 194-210), recomputing P from the GLOBAL lse.
 //
-// One CTA = one 128-row key/value tile of one kv head; it loops over the q heads of its
-// GQA group and the non-SKIP 128-row query tiles, accumulating dK and dV in TMEM.
+// One CTA = one 128-row key/value tile j of one kv head g; it loops over the q heads of its
+// GQA group and the non-SKIP 128-row query tiles i, accumulating dK and dV in TMEM.
 // Transposed orientation (TMEM lane = key row):
-//   S^T  = K Q^T              (SS, both K-major)            -> TMEM [0,128)
-//   dP^T = V dO^T             (SS, both K-major)            -> TMEM [128,256)
-//   P^T  = exp2(S^T*scale*log2e - lse*log2e), dS^T = P^T o (dP^T - dsum)   (compute WG)
-//   dV  += P^T dO             (TS: P^T bf16 in TMEM over S^T; dO MN-major)  -> [256,256+D)
-//   dK  += dS^T Q             (SS: dS^T smem K-major; Q MN-major)           -> [256+D,256+2D)
-//   dQ_i = dS K               (SS: dS = MN-major view of the same smem; K MN-major) -> [128,...)
-// dQ_i is drained by a second warpgroup with fp32 vector atomics into dq_acc; dK/dV are
-// added into the travelling fp32 accumulators once per CTA (the CTA owns those rows).
+//   S^T  = K Q_i^T            (SS, both K-major)                       -> TMEM [0,128)
+//   dP^T = V dO_i^T           (SS, both K-major)                       -> TMEM [128,256)
+//   P^T  = exp2(S^T*scale*log2e - lse*log2e)     (compute WGs, written back as bf16 over S^T)
+//   dV  += P^T dO_i           (TS; dO MN-major)                         -> [256,256+D)
+//   dS^T = P^T o (dP^T - dsum)                    (compute WGs, bf16 into smem, SW128)
+//   dK  += dS^T Q_i           (SS: dS^T K-major; Q MN-major)            -> [256+D,256+2D)
+//   dQ_i = dS K               (SS: dS = MN-major view of the same smem) -> [128,128+D)
+// dQ_i is drained (TMEM -> smem staging in the dS buffer -> TMA bulk reduce-add into the
+// fp32 dq_acc); dK / dV are added into the travelling fp32 accumulators with TMA
+// reduce-add once per CTA (the CTA owns those rows, so that part is deterministic).
 //
-// Warps: 0 TMA producer (+ lse/dsum staging), 1 MMA issuer, 2 TMEM allocator, 3 idle,
-//        4-7 compute (P^T, dS^T) + final dV, 8-11 dQ drain + final dK.
+// Warp groups (512 threads):
+//   WG0: warp 0 TMA producer (+ lse/dsum staging), warp 1 MMA issuer, warp 2 TMEM alloc.
+//   WG1 / WG2: compute, query columns [0,64) / [64,128) of each tile (two warps per SMSP).
+//              Phase P (needs S^T) overlaps the dP^T MMA; phase dS overlaps the dV MMA.
+//   WG3: dQ drain, then the dK epilogue.  WG1 also runs the dV epilogue.
 #include "../../include/striped_attn.h"
 #include "common.cuh"
 #include "internal.h"
 
+#include <cstdlib>
+
 namespace sa {
 namespace {
 
-constexpr uint32_t kPanelBytes = 128 * 128;
+constexpr uint32_t kPanelBytes = 128 * 128;  // 128 rows x 128 B
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct BwdParams {
-  CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq, tk, tv, tdo;   // bf16 [c, H, D], box 64 x 1 x 128
+  CUtensorMap tdq, tdk, tdv;     // fp32 [c, H, D], box 32 x 1 x 128 (reduce-add)
   const float* lse;
   const float* dsum;
-  float* dq;
-  float* dk;
-  float* dv;
   int c, hq, hkv, n_t;
   float scale, scale_log2;
   int kind;
+  int debug;  // perf experiments only: bit0 = skip the dQ reduction
 };
 
 template <int D>
 struct BwdSmem {
-  static constexpr uint32_t kTile = D / 64 * kPanelBytes;
+  static constexpr uint32_t kTile = D / 64 * kPanelBytes;  // 128 rows x D bf16
   static constexpr uint32_t kK = 0, kV = kTile, kQ = 2 * kTile, kDO = 4 * kTile, kDS = 6 * kTile;
   static constexpr uint32_t kLse = kDS + 2 * kPanelBytes;  // 2 stages x 128 fp32
   static constexpr uint32_t kDsum = kLse + 1024;
-  static constexpr uint32_t kBar = kDsum + 1024;  // mbarriers + TMEM address (no static smem)
-  static constexpr uint32_t kBytes = kBar + 128;
+  static constexpr uint32_t kBar = kDsum + 1024;
+  static constexpr uint32_t kBytes = kBar + 256;
   static constexpr uint32_t kAlloc = kBytes + 1024 <= 232448 ? kBytes + 1024 : 232448;
+};
+
+enum : int {
+  B_KV_FULL = 0, B_S_FULL, B_DP_FULL, B_P_READY, B_DS_READY, B_DQ_FULL, B_DQ_FREE, B_DSS_FREE,
+  B_KV_DONE, B_Q_FULL = 9 /* x2 */, B_LSE_FULL = 11 /* x2 */, B_Q_EMPTY = 13 /* x2 */, B_COUNT = 15
 };
 
 __device__ __forceinline__ bool allowed_bwd(int kind, int x, int y, int c) {
@@ -57,20 +68,17 @@ __device__ __forceinline__ bool allowed_bwd(int kind, int x, int y, int c) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(384, 1) bwd_kernel(const __grid_constant__ BwdParams p) {
+__global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ BwdParams p) {
   using L = BwdSmem<D>;
   constexpr int kPanels = D / 64;
   constexpr int kKSteps = D / 16;
+  constexpr int kChunks = D / 32;  // 32-column fp32 chunks of dQ / dK / dV
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kBar);
-  uint64_t &kv_full = bars[0], &st_full = bars[1], &ds_full = bars[2], &ds_empty = bars[3],
-           &dq_full = bars[4], &dq_empty = bars[5], &kv_done = bars[6];
-  uint64_t* q_full = bars + 7;
-  uint64_t* lse_full = bars + 9;
-  uint64_t* q_empty = bars + 11;
-  uint32_t& tmem_base_s = *reinterpret_cast<uint32_t*>(bars + 13);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBar);
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(bar + B_COUNT);
+  const uint32_t sbase = smem_u32(smem);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   if (smem + L::kBytes > smem_raw + L::kAlloc) __trap();  // alignment slack exhausted
@@ -82,71 +90,77 @@ __global__ void __launch_bounds__(384, 1) bwd_kernel(const __grid_constant__ Bwd
   const int i0 = causal ? j : 0;
   const int n_i = p.n_t - i0;
   const int n_it = group * n_i;
-  const float* lse_g = p.lse;
 
-  if (warp == 2) tmem_alloc<512>(&tmem_base_s);
+  if (warp == 2) tmem_alloc<512>(tmem_base_s);
   if (warp == 1 && lane == 0) {
-    mbar_init(&kv_full, 1);
+    mbar_init(&bar[B_KV_FULL], 1);
     for (int s = 0; s < 2; s++) {
-      mbar_init(&q_full[s], 1);
-      mbar_init(&lse_full[s], 32);
-      mbar_init(&q_empty[s], 1);
+      mbar_init(&bar[B_Q_FULL + s], 1);
+      mbar_init(&bar[B_LSE_FULL + s], 32);
+      mbar_init(&bar[B_Q_EMPTY + s], 1);
     }
-    mbar_init(&st_full, 1);
-    mbar_init(&ds_full, 128);
-    mbar_init(&ds_empty, 1);
-    mbar_init(&dq_full, 1);
-    mbar_init(&dq_empty, 128);
-    mbar_init(&kv_done, 1);
+    mbar_init(&bar[B_S_FULL], 1);
+    mbar_init(&bar[B_DP_FULL], 1);
+    mbar_init(&bar[B_P_READY], 256);
+    mbar_init(&bar[B_DS_READY], 256);
+    mbar_init(&bar[B_DQ_FULL], 1);
+    mbar_init(&bar[B_DQ_FREE], 128);
+    mbar_init(&bar[B_DSS_FREE], 1);
+    mbar_init(&bar[B_KV_DONE], 1);
     fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tq);
+    prefetch_tmap(&p.tdo);
+    prefetch_tmap(&p.tdq);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = tmem_base_s;
+  const uint32_t tbase = *tmem_base_s;
   const uint32_t t_st = tbase, t_dpt = tbase + 128, t_dv = tbase + 256, t_dk = tbase + 256 + D;
 
   if (warp < 4) {
-    regs_dec<56>();
+    regs_dec<64>();
     if (warp == 0) {
       // ---------------------------------------------------------- producer
       const uint64_t pol_kv = policy_evict_first(), pol_q = policy_evict_last();
       if (lane == 0) {
-        mbar_arrive_expect_tx(&kv_full, 2 * L::kTile);
+        mbar_arrive_expect_tx(&bar[B_KV_FULL], 2 * L::kTile);
         for (int pn = 0; pn < kPanels; pn++) {
-          tma_load_3d(smem + L::kK + pn * kPanelBytes, &p.tk, &kv_full, 64 * pn, g, 128 * j, pol_kv);
-          tma_load_3d(smem + L::kV + pn * kPanelBytes, &p.tv, &kv_full, 64 * pn, g, 128 * j, pol_kv);
+          tma_load_3d(smem + L::kK + pn * kPanelBytes, &p.tk, &bar[B_KV_FULL], 64 * pn, g, 128 * j,
+                      pol_kv);
+          tma_load_3d(smem + L::kV + pn * kPanelBytes, &p.tv, &bar[B_KV_FULL], 64 * pn, g, 128 * j,
+                      pol_kv);
         }
       }
       for (int it = 0; it < n_it; it++) {
         const int s = it & 1;
         const int h = g * group + it / n_i;
         const int i = i0 + it % n_i;
-        if (it >= 2) mbar_wait(&q_empty[s], ((it >> 1) - 1) & 1);
+        if (it >= 2) mbar_wait(&bar[B_Q_EMPTY + s], ((it >> 1) - 1) & 1);
         if (lane == 0) {
-          mbar_arrive_expect_tx(&q_full[s], 2 * L::kTile);
+          mbar_arrive_expect_tx(&bar[B_Q_FULL + s], 2 * L::kTile);
           for (int pn = 0; pn < kPanels; pn++) {
-            tma_load_3d(smem + L::kQ + s * L::kTile + pn * kPanelBytes, &p.tq, &q_full[s], 64 * pn,
-                        h, 128 * i, pol_q);
-            tma_load_3d(smem + L::kDO + s * L::kTile + pn * kPanelBytes, &p.tdo, &q_full[s],
+            tma_load_3d(smem + L::kQ + s * L::kTile + pn * kPanelBytes, &p.tq, &bar[B_Q_FULL + s],
                         64 * pn, h, 128 * i, pol_q);
+            tma_load_3d(smem + L::kDO + s * L::kTile + pn * kPanelBytes, &p.tdo,
+                        &bar[B_Q_FULL + s], 64 * pn, h, 128 * i, pol_q);
           }
         }
-        float* lse_s = reinterpret_cast<float*>(smem + L::kLse + s * 512);
-        float* dsum_s = reinterpret_cast<float*>(smem + L::kDsum + s * 512);
 #pragma unroll
         for (int e = 0; e < 4; e++) {
           const int xl = lane * 4 + e, x = 128 * i + xl;
-          float lv = INFINITY, dv = 0.f;
+          float lv = INFINITY, dv = 0.f;  // rows past the block: P = 0
           if (x < p.c) {
-            const float raw = lse_g[(int64_t)h * p.c + x];
+            const float raw = p.lse[(int64_t)h * p.c + x];
             lv = raw == -INFINITY ? INFINITY : raw * kLog2e;  // dead row -> P = 0
             dv = p.dsum[(int64_t)h * p.c + x];
           }
-          lse_s[xl] = lv;
-          dsum_s[xl] = dv;
+          sts32f(sbase + L::kLse + s * 512 + xl * 4, lv);
+          sts32f(sbase + L::kDsum + s * 512 + xl * 4, dv);
         }
-        mbar_arrive(&lse_full[s]);
+        mbar_arrive(&bar[B_LSE_FULL + s]);
       }
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
@@ -154,176 +168,223 @@ __global__ void __launch_bounds__(384, 1) bwd_kernel(const __grid_constant__ Bwd
         const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
         const uint32_t id_kv = idesc_bf16(128, D, 0, 1);
         const uint32_t id_q = idesc_bf16(128, D, 1, 1);
-        const uint32_t k_addr = smem_u32(smem + L::kK), v_addr = smem_u32(smem + L::kV);
-        const uint32_t ds_addr = smem_u32(smem + L::kDS);
-        mbar_wait(&kv_full, 0);
+        const uint32_t k_addr = sbase + L::kK, v_addr = sbase + L::kV, ds_addr = sbase + L::kDS;
+        mbar_wait(&bar[B_KV_FULL], 0);
         for (int it = 0; it < n_it; it++) {
           const int s = it & 1;
-          const uint32_t q_addr = smem_u32(smem + L::kQ + s * L::kTile);
-          const uint32_t do_addr = smem_u32(smem + L::kDO + s * L::kTile);
-          mbar_wait(&q_full[s], (it >> 1) & 1);
+          const uint32_t q_addr = sbase + L::kQ + s * L::kTile;
+          const uint32_t do_addr = sbase + L::kDO + s * L::kTile;
+          mbar_wait(&bar[B_Q_FULL + s], (it >> 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < kKSteps; kk++) {
             const uint32_t off = (kk >> 2) * kPanelBytes + (kk & 3) * 32;
             mma_ss(t_st, sdesc(k_addr + off, 16, 1024), sdesc(q_addr + off, 16, 1024), id_s, kk > 0);
           }
+          mma_commit(&bar[B_S_FULL]);
           if (it > 0) {
-            mbar_wait(&dq_empty, (it - 1) & 1);
+            mbar_wait(&bar[B_DQ_FREE], (it - 1) & 1);
             tc_fence_after();
           }
 #pragma unroll
           for (int kk = 0; kk < kKSteps; kk++) {
             const uint32_t off = (kk >> 2) * kPanelBytes + (kk & 3) * 32;
-            mma_ss(t_dpt, sdesc(v_addr + off, 16, 1024), sdesc(do_addr + off, 16, 1024), id_s, kk > 0);
+            mma_ss(t_dpt, sdesc(v_addr + off, 16, 1024), sdesc(do_addr + off, 16, 1024), id_s,
+                   kk > 0);
           }
-          mma_commit(&st_full);
-          mbar_wait(&ds_full, it & 1);
+          mma_commit(&bar[B_DP_FULL]);
+          mbar_wait(&bar[B_P_READY], it & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; kk++)  // P^T: q cols [0,64) at TMEM [0,32), [64,128) at [64,96)
+            mma_ts(t_dv, t_st + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
+                   sdesc(do_addr + kk * 2048, kPanelBytes, 1024), id_kv,
+                   (it > 0 || kk > 0) ? 1u : 0u);
+          mbar_wait(&bar[B_DS_READY], it & 1);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 8; kk++)
-            mma_ts(t_dv, t_st + kk * 8, sdesc(do_addr + kk * 2048, kPanelBytes, 1024), id_kv,
-                   (it > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < 8; kk++)
             mma_ss(t_dk, sdesc(ds_addr + (kk >> 2) * kPanelBytes + (kk & 3) * 32, 16, 1024),
-                   sdesc(q_addr + kk * 2048, kPanelBytes, 1024), id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+                   sdesc(q_addr + kk * 2048, kPanelBytes, 1024), id_kv,
+                   (it > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
           for (int kk = 0; kk < 8; kk++)
             mma_ss(t_dpt, sdesc(ds_addr + kk * 2048, kPanelBytes, 1024),
                    sdesc(k_addr + kk * 2048, kPanelBytes, 1024), id_q, kk > 0);
-          mma_commit(&dq_full);
-          mma_commit(&ds_empty);
-          mma_commit(&q_empty[s]);
+          mma_commit(&bar[B_DQ_FULL]);
+          mma_commit(&bar[B_Q_EMPTY + s]);
         }
-        mma_commit(&kv_done);
+        mma_commit(&bar[B_KV_DONE]);
       }
     }
-  } else {
-    regs_inc<224>();
+  } else if (warp < 12) {
+    regs_inc<160>();
+    // ------------------------------------------------------------ compute WGs
+    const int half = (warp - 4) >> 2;  // query columns [64*half, 64*half + 64)
     const uint32_t row = (warp & 3) * 32 + lane;
     const uint32_t lane_off = ((warp & 3) * 32) << 16;
-    const int y = 128 * j + row;  // key row (compute WG) / query row within tile (dQ WG)
-    if (warp < 8) {
-      // ---------------------------------------------------------- compute WG: P^T, dS^T
-      uint8_t* ds_smem = smem + L::kDS;
-      for (int it = 0; it < n_it; it++) {
-        const int s = it & 1;
-        const int i = i0 + it % n_i;
-        mbar_wait(&st_full, it & 1);
-        tc_fence_after();
-        mbar_wait(&lse_full[s], (it >> 1) & 1);
-        if (it > 0) mbar_wait(&ds_empty, (it - 1) & 1);
-        const float* lse_s = reinterpret_cast<const float*>(smem + L::kLse + s * 512);
-        const float* dsum_s = reinterpret_cast<const float*>(smem + L::kDsum + s * 512);
-        const bool masked = (causal && i == j) || (i + 1) * 128 > p.c || (j + 1) * 128 > p.c;
-#pragma unroll 1
-        for (int ch = 0; ch < 4; ch++) {
-          uint32_t sr[32], dr[32];
-          SA_TMEM_LD32(t_st + lane_off + ch * 32, sr);
-          SA_TMEM_LD32(t_dpt + lane_off + ch * 32, dr);
-          tmem_ld_wait();
-          uint32_t pk[16], dk[16];
-#pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float pp[2], dd[2];
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-              const int xl = ch * 32 + e + u;
-              float pv = ex2(fmaf(__uint_as_float(sr[e + u]), p.scale_log2, -lse_s[xl]));
-              if (masked && !allowed_bwd(p.kind, 128 * i + xl, y, p.c)) pv = 0.f;
-              pp[u] = pv;
-              dd[u] = pv * (__uint_as_float(dr[e + u]) - dsum_s[xl]);
-            }
-            pk[e / 2] = pack_bf16(pp[0], pp[1]);
-            dk[e / 2] = pack_bf16(dd[0], dd[1]);
-          }
-          SA_TMEM_ST16(t_st + lane_off + ch * 16, pk);
-          // dS^T row `row`, query columns [32ch, 32ch+32): panel ch/2, 16B chunks (ch&1)*4 + q
-          uint8_t* panel = ds_smem + (ch >> 1) * kPanelBytes;
-#pragma unroll
-          for (int qd = 0; qd < 4; qd++) {
-            const uint32_t off = sw128_off(row, (ch & 1) * 4 + qd);
-            *reinterpret_cast<uint4*>(panel + off) =
-                make_uint4(dk[4 * qd], dk[4 * qd + 1], dk[4 * qd + 2], dk[4 * qd + 3]);
-          }
-        }
-        tmem_st_wait();
-        fence_proxy_async_smem();
-        tc_fence_before();
-        mbar_arrive(&ds_full);
-      }
-      // final dV (this CTA owns key rows [128j, 128j+128) of kv head g)
-      mbar_wait(&kv_done, 0);
+    const int y = 128 * j + row;
+    const uint32_t ds_panel = sbase + L::kDS + half * kPanelBytes;
+    for (int it = 0; it < n_it; it++) {
+      const int s = it & 1;
+      const int i = i0 + it % n_i;
+      const bool masked = (causal && i == j) || (i + 1) * 128 > p.c || (j + 1) * 128 > p.c;
+      const uint32_t lse_a = sbase + L::kLse + s * 512 + half * 256;
+      const uint32_t dsum_a = sbase + L::kDsum + s * 512 + half * 256;
+      const int xbase = 128 * i + 64 * half;
+      mbar_wait(&bar[B_S_FULL], it & 1);
       tc_fence_after();
-      const int64_t base = ((int64_t)y * p.hkv + g) * D;
+      mbar_wait(&bar[B_LSE_FULL + s], (it >> 1) & 1);
+      float pv[64];
+#pragma unroll
+      for (int ch = 0; ch < 2; ch++) {
+        uint32_t sr[32];
+        SA_TMEM_LD32(t_st + lane_off + half * 64 + ch * 32, sr);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 l4 = lds128f(lse_a + (ch * 32 + e) * 4);
+          pv[ch * 32 + e + 0] = ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x));
+          pv[ch * 32 + e + 1] = ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y));
+          pv[ch * 32 + e + 2] = ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z));
+          pv[ch * 32 + e + 3] = ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w));
+        }
+        if (masked) {
+#pragma unroll
+          for (int e = 0; e < 32; e++)
+            if (!allowed_bwd(p.kind, xbase + ch * 32 + e, y, p.c)) pv[ch * 32 + e] = 0.f;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; e++) pk[e] = pack_bf16(pv[ch * 32 + 2 * e], pv[ch * 32 + 2 * e + 1]);
+        SA_TMEM_ST16(t_st + lane_off + half * 64 + ch * 16, pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bar[B_P_READY]);
+
+      mbar_wait(&bar[B_DP_FULL], it & 1);
+      tc_fence_after();
+      if (it > 0) mbar_wait(&bar[B_DSS_FREE], (it - 1) & 1);
+#pragma unroll
+      for (int ch = 0; ch < 2; ch++) {
+        uint32_t dr[32];
+        SA_TMEM_LD32(t_dpt + lane_off + half * 64 + ch * 32, dr);
+        tmem_ld_wait();
+        uint32_t dk[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float4 d4 = lds128f(dsum_a + (ch * 32 + e) * 4);
+          const float a0 = pv[ch * 32 + e + 0] * (__uint_as_float(dr[e + 0]) - d4.x);
+          const float a1 = pv[ch * 32 + e + 1] * (__uint_as_float(dr[e + 1]) - d4.y);
+          const float a2 = pv[ch * 32 + e + 2] * (__uint_as_float(dr[e + 2]) - d4.z);
+          const float a3 = pv[ch * 32 + e + 3] * (__uint_as_float(dr[e + 3]) - d4.w);
+          dk[e / 2] = pack_bf16(a0, a1);
+          dk[e / 2 + 1] = pack_bf16(a2, a3);
+        }
+        // dS^T row `row`, this half's query columns [32ch, 32ch+32) -> 16 B chunks 4ch..4ch+3
+#pragma unroll
+        for (int qd = 0; qd < 4; qd++)
+          sts128(ds_panel + sw128_off(row, ch * 4 + qd), dk[4 * qd], dk[4 * qd + 1], dk[4 * qd + 2],
+                 dk[4 * qd + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bar[B_DS_READY]);
+    }
+    if (half == 0) {
+      // ---------------------------------------------------------- dV epilogue
+      mbar_wait(&bar[B_KV_DONE], 0);
+      tc_fence_after();
+      const uint32_t stage = sbase + L::kQ;  // Q stages are free now
 #pragma unroll 1
-      for (int ch = 0; ch < D / 32; ch++) {
+      for (int ch = 0; ch < kChunks; ch++) {
         uint32_t o[32];
         SA_TMEM_LD32(t_dv + lane_off + ch * 32, o);
         tmem_ld_wait();
-        if (y < p.c) {
-          float4* dst = reinterpret_cast<float4*>(p.dv + base + ch * 32);
 #pragma unroll
-          for (int e = 0; e < 8; e++) {
-            float4 a = dst[e];
-            a.x += __uint_as_float(o[4 * e]);
-            a.y += __uint_as_float(o[4 * e + 1]);
-            a.z += __uint_as_float(o[4 * e + 2]);
-            a.w += __uint_as_float(o[4 * e + 3]);
-            dst[e] = a;
-          }
-        }
+        for (int qd = 0; qd < 8; qd++)
+          sts128(stage + ch * kPanelBytes + sw128_off(row, qd), o[4 * qd], o[4 * qd + 1],
+                 o[4 * qd + 2], o[4 * qd + 3]);
       }
-    } else {
-      // ---------------------------------------------------------- dQ drain WG
-      for (int it = 0; it < n_it; it++) {
-        const int h = g * group + it / n_i;
-        const int i = i0 + it % n_i;
-        mbar_wait(&dq_full, it & 1);
-        tc_fence_after();
-        const int x = 128 * i + row;
-        float* dst = p.dq + ((int64_t)x * p.hq + h) * D;
-#pragma unroll 1
-        for (int ch = 0; ch < D / 32; ch++) {
-          uint32_t o[32];
-          SA_TMEM_LD32(t_dpt + lane_off + ch * 32, o);
-          tmem_ld_wait();
-          if (x < p.c) {
-#pragma unroll
-            for (int e = 0; e < 8; e++)
-              atomicAdd(reinterpret_cast<float4*>(dst + ch * 32 + 4 * e),
-                        make_float4(__uint_as_float(o[4 * e]) * p.scale,
-                                    __uint_as_float(o[4 * e + 1]) * p.scale,
-                                    __uint_as_float(o[4 * e + 2]) * p.scale,
-                                    __uint_as_float(o[4 * e + 3]) * p.scale));
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&dq_empty);
+      fence_proxy_async_smem();
+      named_bar_sync(2, 128);
+      if (warp == 4 && lane == 0) {
+        for (int ch = 0; ch < kChunks; ch++)
+          tma_reduce_add_3d(&p.tdv, smem + L::kQ + ch * kPanelBytes, 32 * ch, g, 128 * j);
+        bulk_commit();
+        bulk_wait<0>();
       }
-      // final dK
-      mbar_wait(&kv_done, 0);
+    }
+  } else {
+    regs_inc<128>();
+    // ------------------------------------------------------------ dQ drain + dK epilogue
+    const uint32_t row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = ((warp & 3) * 32) << 16;
+    const bool leader = warp == 12 && lane == 0;
+    const uint32_t stage = sbase + L::kDS;  // dS buffer doubles as dQ staging (2 x 16 KB)
+    for (int it = 0; it < n_it; it++) {
+      const int h = g * group + it / n_i;
+      const int i = i0 + it % n_i;
+      mbar_wait(&bar[B_DQ_FULL], it & 1);
       tc_fence_after();
-      const int64_t base = ((int64_t)y * p.hkv + g) * D;
 #pragma unroll 1
-      for (int ch = 0; ch < D / 32; ch++) {
+      for (int ch = 0; ch < kChunks; ch++) {
         uint32_t o[32];
-        SA_TMEM_LD32(t_dk + lane_off + ch * 32, o);
+        SA_TMEM_LD32(t_dpt + lane_off + ch * 32, o);
         tmem_ld_wait();
-        if (y < p.c) {
-          float4* dst = reinterpret_cast<float4*>(p.dk + base + ch * 32);
+        if (ch == kChunks - 1) {
+          tc_fence_before();
+          mbar_arrive(&bar[B_DQ_FREE]);
+        }
+        if (p.debug & 1) continue;
+        const uint32_t buf = stage + (ch & 1) * kPanelBytes;
+        if (ch >= 2) {
+          if (leader) bulk_wait_read<1>();
+          named_bar_sync(1, 128);
+        }
 #pragma unroll
-          for (int e = 0; e < 8; e++) {
-            float4 a = dst[e];
-            a.x += __uint_as_float(o[4 * e]) * p.scale;
-            a.y += __uint_as_float(o[4 * e + 1]) * p.scale;
-            a.z += __uint_as_float(o[4 * e + 2]) * p.scale;
-            a.w += __uint_as_float(o[4 * e + 3]) * p.scale;
-            dst[e] = a;
-          }
+        for (int qd = 0; qd < 8; qd++)
+          sts128(buf + sw128_off(row, qd), __float_as_uint(__uint_as_float(o[4 * qd]) * p.scale),
+                 __float_as_uint(__uint_as_float(o[4 * qd + 1]) * p.scale),
+                 __float_as_uint(__uint_as_float(o[4 * qd + 2]) * p.scale),
+                 __float_as_uint(__uint_as_float(o[4 * qd + 3]) * p.scale));
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (leader) {
+          tma_reduce_add_3d(&p.tdq, smem + L::kDS + (ch & 1) * kPanelBytes, 32 * ch, h, 128 * i);
+          bulk_commit();
         }
       }
+      if (leader) {
+        bulk_wait_read<0>();
+        mbar_arrive(&bar[B_DSS_FREE]);
+      }
+    }
+    // ------------------------------------------------------------ dK epilogue
+    mbar_wait(&bar[B_KV_DONE], 0);
+    tc_fence_after();
+    const uint32_t kst = sbase + L::kDO;  // dO stages are free now
+#pragma unroll 1
+    for (int ch = 0; ch < kChunks; ch++) {
+      uint32_t o[32];
+      SA_TMEM_LD32(t_dk + lane_off + ch * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int qd = 0; qd < 8; qd++)
+        sts128(kst + ch * kPanelBytes + sw128_off(row, qd),
+               __float_as_uint(__uint_as_float(o[4 * qd]) * p.scale),
+               __float_as_uint(__uint_as_float(o[4 * qd + 1]) * p.scale),
+               __float_as_uint(__uint_as_float(o[4 * qd + 2]) * p.scale),
+               __float_as_uint(__uint_as_float(o[4 * qd + 3]) * p.scale));
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (leader) {
+      for (int ch = 0; ch < kChunks; ch++)
+        tma_reduce_add_3d(&p.tdk, smem + L::kDO + ch * kPanelBytes, 32 * ch, g, 128 * j);
+      bulk_commit();
+      bulk_wait<0>();
     }
   }
   tc_fence_before();
@@ -342,7 +403,7 @@ int launch_bwd_d(BwdParams& prm, cudaStream_t st) {
     cudaFuncSetAttribute(bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr_set = true;
   }
-  bwd_kernel<D><<<prm.n_t * prm.hkv, 384, smem, st>>>(prm);
+  bwd_kernel<D><<<prm.n_t * prm.hkv, 512, smem, st>>>(prm);
   return check_launch("bwd_kernel");
 }
 
@@ -356,11 +417,11 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   if (int r = make_tmap_rows(&prm.tk, k, c, hkv, d, 128)) return r;
   if (int r = make_tmap_rows(&prm.tv, v, c, hkv, d, 128)) return r;
   if (int r = make_tmap_rows(&prm.tdo, dout, c, hq, d, 128)) return r;
+  if (int r = make_tmap_rows_f32(&prm.tdq, dq, c, hq, d, 128)) return r;
+  if (int r = make_tmap_rows_f32(&prm.tdk, dk, c, hkv, d, 128)) return r;
+  if (int r = make_tmap_rows_f32(&prm.tdv, dv, c, hkv, d, 128)) return r;
   prm.lse = lse;
   prm.dsum = dsum;
-  prm.dq = dq;
-  prm.dk = dk;
-  prm.dv = dv;
   prm.c = static_cast<int>(c);
   prm.hq = hq;
   prm.hkv = hkv;
@@ -368,6 +429,8 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   prm.scale = scale;
   prm.scale_log2 = scale * kLog2e;
   prm.kind = kind;
+  const char* dbg = getenv("SA_BWD_DEBUG");
+  prm.debug = dbg ? atoi(dbg) : 0;
   return d == 128 ? launch_bwd_d<128>(prm, st) : launch_bwd_d<64>(prm, st);
 }
 

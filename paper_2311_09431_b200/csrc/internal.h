@@ -16,6 +16,9 @@ void count_launch(int n = 1);
 // (64 x 1 x box_rows) box and 128-byte swizzle (one smem "panel" per box).
 int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int32_t heads, int32_t dim,
                    int32_t box_rows);
+// fp32 [rows, heads, dim] map, box (32 x 1 x box_rows), SW128 (accumulator TMA reduce-add).
+int make_tmap_rows_f32(CUtensorMap* map, const void* base, int64_t rows, int32_t heads,
+                       int32_t dim, int32_t box_rows);
 // 2-D bf16 [rows, cols] map, box (64 x box_rows), SW128 (probe kernel).
 int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int32_t box_rows);
 
