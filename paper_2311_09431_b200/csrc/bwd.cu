@@ -12,19 +12,27 @@
 //   dS^T = P^T o (dP^T - dsum)                    (compute WGs, bf16 into smem, SW128)
 //   dK  += dS^T Q_i           (SS: dS^T K-major; Q MN-major)            -> [256+D,256+2D)
 //   dQ_i = dS K               (SS: dS = MN-major view of the same smem) -> [128,128+D)
-// dQ_i is drained (TMEM -> smem staging in the dS buffer -> TMA bulk reduce-add into the
-// fp32 dq_acc); dK / dV are added into the travelling fp32 accumulators with TMA
-// reduce-add once per CTA (the CTA owns those rows, so that part is deterministic).
+// dQ_i is drained TMEM -> registers -> a dedicated smem staging buffer -> TMA bulk
+// reduce-add into the fp32 dq_acc; dK / dV are added into the travelling fp32 accumulators
+// with TMA reduce-add once per CTA (the CTA owns those rows: deterministic).
+//
+// MMA issue order (one elected lane of warp 1):
+//   prologue S(0) dP(0);  per i:  [P(i)] dV(i)  [Q(i+1)] S(i+1)  [dS(i)] dQ(i) dK(i)
+//                                 [dQ(i) drained, dO(i+1)] dP(i+1)
+// so the compute warpgroups run P(i+1) right after dS(i) while the tensor core works
+// through dQ(i), dK(i), dP(i+1): the two sides overlap instead of alternating.
 //
 // Warp groups (512 threads):
 //   WG0: warp 0 TMA producer (+ lse/dsum staging), warp 1 MMA issuer, warp 2 TMEM alloc.
 //   WG1 / WG2: compute, query columns [0,64) / [64,128) of each tile (two warps per SMSP).
-//              Phase P (needs S^T) overlaps the dP^T MMA; phase dS overlaps the dV MMA.
 //   WG3: dQ drain, then the dK epilogue.  WG1 also runs the dV epilogue.
+// Shared memory (D=128): K, V 32 KB each; Q 2 stages; dO 1 stage (refilled as soon as
+// dV(i) retires); dS 32 KB; dQ staging 2 x 16 KB; lse / dsum 2 stages.
 #include "../../include/striped_attn.h"
 #include "common.cuh"
 #include "internal.h"
 
+#include <cstdio>
 #include <cstdlib>
 
 namespace sa {
@@ -41,14 +49,22 @@ struct BwdParams {
   int c, hq, hkv, n_t;
   float scale, scale_log2;
   int kind;
-  int debug;  // perf experiments only: bit0 = skip the dQ reduction
+  int debug;         // perf experiments only: bit0 = skip the dQ reduction
+  long long* trace;  // perf experiments only: per-iteration clock64 stamps of one CTA
+  int trace_cta;
 };
+
+#define SA_TR(slot)                                                                     \
+  do {                                                                                  \
+    if (p.trace && blockIdx.x == p.trace_cta && it < 16) p.trace[it * 32 + (slot)] = clock64(); \
+  } while (0)
 
 template <int D>
 struct BwdSmem {
   static constexpr uint32_t kTile = D / 64 * kPanelBytes;  // 128 rows x D bf16
-  static constexpr uint32_t kK = 0, kV = kTile, kQ = 2 * kTile, kDO = 4 * kTile, kDS = 6 * kTile;
-  static constexpr uint32_t kLse = kDS + 2 * kPanelBytes;  // 2 stages x 128 fp32
+  static constexpr uint32_t kK = 0, kV = kTile, kQ = 2 * kTile, kDO = 4 * kTile, kDS = 5 * kTile;
+  static constexpr uint32_t kStg = kDS + 2 * kPanelBytes;   // dQ staging, 2 x 16 KB
+  static constexpr uint32_t kLse = kStg + 2 * kPanelBytes;  // 2 stages x 128 fp32
   static constexpr uint32_t kDsum = kLse + 1024;
   static constexpr uint32_t kBar = kDsum + 1024;
   static constexpr uint32_t kBytes = kBar + 256;
@@ -56,8 +72,9 @@ struct BwdSmem {
 };
 
 enum : int {
-  B_KV_FULL = 0, B_S_FULL, B_DP_FULL, B_P_READY, B_DS_READY, B_DQ_FULL, B_DQ_FREE, B_DSS_FREE,
-  B_KV_DONE, B_Q_FULL = 9 /* x2 */, B_LSE_FULL = 11 /* x2 */, B_Q_EMPTY = 13 /* x2 */, B_COUNT = 15
+  B_KV_FULL = 0, B_S_FULL, B_DP_FULL, B_P_READY, B_DS_READY, B_DQ_FULL, B_DQ_FREE, B_DS_EMPTY,
+  B_KV_DONE, B_DO_FULL, B_DO_EMPTY, B_Q_FULL = 11 /* x2 */, B_LSE_FULL = 13 /* x2 */,
+  B_Q_EMPTY = 15 /* x2 */, B_COUNT = 17
 };
 
 __device__ __forceinline__ bool allowed_bwd(int kind, int x, int y, int c) {
@@ -93,20 +110,12 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
 
   if (warp == 2) tmem_alloc<512>(tmem_base_s);
   if (warp == 1 && lane == 0) {
-    mbar_init(&bar[B_KV_FULL], 1);
-    for (int s = 0; s < 2; s++) {
-      mbar_init(&bar[B_Q_FULL + s], 1);
-      mbar_init(&bar[B_LSE_FULL + s], 32);
-      mbar_init(&bar[B_Q_EMPTY + s], 1);
-    }
-    mbar_init(&bar[B_S_FULL], 1);
-    mbar_init(&bar[B_DP_FULL], 1);
+    for (int b = 0; b < B_COUNT; b++) mbar_init(&bar[b], 1);
+    mbar_init(&bar[B_LSE_FULL], 32);
+    mbar_init(&bar[B_LSE_FULL + 1], 32);
     mbar_init(&bar[B_P_READY], 256);
     mbar_init(&bar[B_DS_READY], 256);
-    mbar_init(&bar[B_DQ_FULL], 1);
     mbar_init(&bar[B_DQ_FREE], 128);
-    mbar_init(&bar[B_DSS_FREE], 1);
-    mbar_init(&bar[B_KV_DONE], 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -121,7 +130,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
   const uint32_t t_st = tbase, t_dpt = tbase + 128, t_dv = tbase + 256, t_dk = tbase + 256 + D;
 
   if (warp < 4) {
-    regs_dec<64>();
+    regs_dec<56>();
     if (warp == 0) {
       // ---------------------------------------------------------- producer
       const uint64_t pol_kv = policy_evict_first(), pol_q = policy_evict_last();
@@ -138,15 +147,14 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         const int s = it & 1;
         const int h = g * group + it / n_i;
         const int i = i0 + it % n_i;
+        // Q_i (2 stages) and lse/dsum (2 stages): free once dK(i-2) retired
         if (it >= 2) mbar_wait(&bar[B_Q_EMPTY + s], ((it >> 1) - 1) & 1);
         if (lane == 0) {
-          mbar_arrive_expect_tx(&bar[B_Q_FULL + s], 2 * L::kTile);
-          for (int pn = 0; pn < kPanels; pn++) {
+          SA_TR(21);
+          mbar_arrive_expect_tx(&bar[B_Q_FULL + s], L::kTile);
+          for (int pn = 0; pn < kPanels; pn++)
             tma_load_3d(smem + L::kQ + s * L::kTile + pn * kPanelBytes, &p.tq, &bar[B_Q_FULL + s],
                         64 * pn, h, 128 * i, pol_q);
-            tma_load_3d(smem + L::kDO + s * L::kTile + pn * kPanelBytes, &p.tdo,
-                        &bar[B_Q_FULL + s], 64 * pn, h, 128 * i, pol_q);
-          }
         }
 #pragma unroll
         for (int e = 0; e < 4; e++) {
@@ -161,70 +169,118 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
           sts32f(sbase + L::kDsum + s * 512 + xl * 4, dv);
         }
         mbar_arrive(&bar[B_LSE_FULL + s]);
+        // dO_i (single buffer): free once dV(i-1) retired
+        if (it >= 1) mbar_wait(&bar[B_DO_EMPTY], (it - 1) & 1);
+        if (lane == 0) {
+          SA_TR(22);
+          mbar_arrive_expect_tx(&bar[B_DO_FULL], L::kTile);
+          for (int pn = 0; pn < kPanels; pn++)
+            tma_load_3d(smem + L::kDO + pn * kPanelBytes, &p.tdo, &bar[B_DO_FULL], 64 * pn, h,
+                        128 * i, pol_q);
+        }
       }
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
-      if (lane == 0) {
-        const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
-        const uint32_t id_kv = idesc_bf16(128, D, 0, 1);
-        const uint32_t id_q = idesc_bf16(128, D, 1, 1);
-        const uint32_t k_addr = sbase + L::kK, v_addr = sbase + L::kV, ds_addr = sbase + L::kDS;
-        mbar_wait(&bar[B_KV_FULL], 0);
-        for (int it = 0; it < n_it; it++) {
-          const int s = it & 1;
-          const uint32_t q_addr = sbase + L::kQ + s * L::kTile;
-          const uint32_t do_addr = sbase + L::kDO + s * L::kTile;
-          mbar_wait(&bar[B_Q_FULL + s], (it >> 1) & 1);
-          tc_fence_after();
+      // The whole warp walks the schedule (descriptor words stay warp-uniform); one elected
+      // lane issues.  Descriptor lo words: start >> 4 | LBO >> 4 << 16; hi word is shared.
+      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_kv = idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t id_q = idesc_bf16(128, D, 1, 1);
+      constexpr uint32_t hi = sdesc_hi(1024);
+      const uint32_t k_km = sdesc_lo(sbase + L::kK, 16), v_km = sdesc_lo(sbase + L::kV, 16);
+      const uint32_t k_mn = sdesc_lo(sbase + L::kK, kPanelBytes);
+      const uint32_t do_km = sdesc_lo(sbase + L::kDO, 16);
+      const uint32_t do_mn = sdesc_lo(sbase + L::kDO, kPanelBytes);
+      const uint32_t ds_km = sdesc_lo(sbase + L::kDS, 16);
+      const uint32_t ds_mn = sdesc_lo(sbase + L::kDS, kPanelBytes);
+      auto kmaj = [](int kk) -> uint32_t {  // k-step offset inside K-major SW128 panels (16 B units)
+        return ((kk >> 2) * kPanelBytes + (kk & 3) * 32) >> 4;
+      };
+      auto issue_s = [&](int it) {  // S^T(it) = K Q_it^T
+        const int s = it & 1;
+        mbar_wait(&bar[B_Q_FULL + s], (it >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a = opaque(k_km), b = opaque(sdesc_lo(sbase + L::kQ + s * L::kTile, 16));
 #pragma unroll
-          for (int kk = 0; kk < kKSteps; kk++) {
-            const uint32_t off = (kk >> 2) * kPanelBytes + (kk & 3) * 32;
-            mma_ss(t_st, sdesc(k_addr + off, 16, 1024), sdesc(q_addr + off, 16, 1024), id_s, kk > 0);
-          }
+          for (int kk = 0; kk < kKSteps; kk++)
+            mma_ss2(t_st, a + kmaj(kk), hi, b + kmaj(kk), hi, id_s, kk > 0);
           mma_commit(&bar[B_S_FULL]);
-          if (it > 0) {
-            mbar_wait(&bar[B_DQ_FREE], (it - 1) & 1);
-            tc_fence_after();
-          }
+        }
+        __syncwarp();
+        SA_TR(1);
+      };
+      auto issue_dp = [&](int it) {  // dP^T(it) = V dO_it^T, once dQ(it-1) left TMEM
+        mbar_wait(&bar[B_DO_FULL], it & 1);
+        if (it > 0) mbar_wait(&bar[B_DQ_FREE], (it - 1) & 1);
+        SA_TR(2);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a = opaque(v_km), b = opaque(do_km);
 #pragma unroll
-          for (int kk = 0; kk < kKSteps; kk++) {
-            const uint32_t off = (kk >> 2) * kPanelBytes + (kk & 3) * 32;
-            mma_ss(t_dpt, sdesc(v_addr + off, 16, 1024), sdesc(do_addr + off, 16, 1024), id_s,
-                   kk > 0);
-          }
+          for (int kk = 0; kk < kKSteps; kk++)
+            mma_ss2(t_dpt, a + kmaj(kk), hi, b + kmaj(kk), hi, id_s, kk > 0);
           mma_commit(&bar[B_DP_FULL]);
-          mbar_wait(&bar[B_P_READY], it & 1);
-          tc_fence_after();
+        }
+        __syncwarp();
+        SA_TR(3);
+      };
+      mbar_wait(&bar[B_KV_FULL], 0);
+      {
+        const int it = 0;
+        SA_TR(0);
+      }
+      issue_s(0);
+      issue_dp(0);
+      for (int it = 0; it < n_it; it++) {
+        const int s = it & 1;
+        mbar_wait(&bar[B_P_READY], it & 1);
+        SA_TR(4);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t b = opaque(do_mn);
 #pragma unroll
           for (int kk = 0; kk < 8; kk++)  // P^T: q cols [0,64) at TMEM [0,32), [64,128) at [64,96)
-            mma_ts(t_dv, t_st + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8),
-                   sdesc(do_addr + kk * 2048, kPanelBytes, 1024), id_kv,
-                   (it > 0 || kk > 0) ? 1u : 0u);
-          mbar_wait(&bar[B_DS_READY], it & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < 8; kk++)
-            mma_ss(t_dk, sdesc(ds_addr + (kk >> 2) * kPanelBytes + (kk & 3) * 32, 16, 1024),
-                   sdesc(q_addr + kk * 2048, kPanelBytes, 1024), id_kv,
-                   (it > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < 8; kk++)
-            mma_ss(t_dpt, sdesc(ds_addr + kk * 2048, kPanelBytes, 1024),
-                   sdesc(k_addr + kk * 2048, kPanelBytes, 1024), id_q, kk > 0);
-          mma_commit(&bar[B_DQ_FULL]);
-          mma_commit(&bar[B_Q_EMPTY + s]);
+            mma_ts2(t_dv, t_st + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8), b + kk * 128, hi, id_kv,
+                    (it > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&bar[B_DO_EMPTY]);
         }
-        mma_commit(&bar[B_KV_DONE]);
+        __syncwarp();
+        SA_TR(5);
+        if (it + 1 < n_it) issue_s(it + 1);  // S^T cols are free once dV(it) read P^T
+        mbar_wait(&bar[B_DS_READY], it & 1);
+        SA_TR(6);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a = opaque(ds_mn), b = opaque(k_mn);
+#pragma unroll
+          for (int kk = 0; kk < 8; kk++)  // MN-major k-step = 16 rows = 2048 B = 128 units
+            mma_ss2(t_dpt, a + kk * 128, hi, b + kk * 128, hi, id_q, kk > 0);
+          mma_commit(&bar[B_DQ_FULL]);
+          const uint32_t c = opaque(ds_km),
+                         e = opaque(sdesc_lo(sbase + L::kQ + s * L::kTile, kPanelBytes));
+#pragma unroll
+          for (int kk = 0; kk < 8; kk++)
+            mma_ss2(t_dk, c + kmaj(kk), hi, e + kk * 128, hi, id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&bar[B_Q_EMPTY + s]);
+          mma_commit(&bar[B_DS_EMPTY]);
+        }
+        __syncwarp();
+        SA_TR(7);
+        if (it + 1 < n_it) issue_dp(it + 1);
       }
+      if (elect_one()) mma_commit(&bar[B_KV_DONE]);
+      __syncwarp();
     }
   } else if (warp < 12) {
-    regs_inc<160>();
+    regs_inc<152>();
     // ------------------------------------------------------------ compute WGs
     const int half = (warp - 4) >> 2;  // query columns [64*half, 64*half + 64)
     const uint32_t row = (warp & 3) * 32 + lane;
     const uint32_t lane_off = ((warp & 3) * 32) << 16;
     const int y = 128 * j + row;
     const uint32_t ds_panel = sbase + L::kDS + half * kPanelBytes;
+    const bool tr = lane == 0 && warp == 4;
     for (int it = 0; it < n_it; it++) {
       const int s = it & 1;
       const int i = i0 + it % n_i;
@@ -233,6 +289,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       const uint32_t dsum_a = sbase + L::kDsum + s * 512 + half * 256;
       const int xbase = 128 * i + 64 * half;
       mbar_wait(&bar[B_S_FULL], it & 1);
+      if (tr) SA_TR(8);
       tc_fence_after();
       mbar_wait(&bar[B_LSE_FULL + s], (it >> 1) & 1);
       float pv[64];
@@ -262,10 +319,13 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bar[B_P_READY]);
+      if (tr) SA_TR(10);
 
       mbar_wait(&bar[B_DP_FULL], it & 1);
+      if (tr) SA_TR(11);
       tc_fence_after();
-      if (it > 0) mbar_wait(&bar[B_DSS_FREE], (it - 1) & 1);
+      if (it > 0) mbar_wait(&bar[B_DS_EMPTY], (it - 1) & 1);  // dQ/dK(it-1) read dS^T
+      if (tr) SA_TR(12);
 #pragma unroll
       for (int ch = 0; ch < 2; ch++) {
         uint32_t dr[32];
@@ -291,6 +351,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(&bar[B_DS_READY]);
+      if (tr) SA_TR(13);
     }
     if (half == 0) {
       // ---------------------------------------------------------- dV epilogue
@@ -317,54 +378,51 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       }
     }
   } else {
-    regs_inc<128>();
+    regs_inc<152>();
     // ------------------------------------------------------------ dQ drain + dK epilogue
     const uint32_t row = (warp & 3) * 32 + lane;
     const uint32_t lane_off = ((warp & 3) * 32) << 16;
     const bool leader = warp == 12 && lane == 0;
-    const uint32_t stage = sbase + L::kDS;  // dS buffer doubles as dQ staging (2 x 16 KB)
     for (int it = 0; it < n_it; it++) {
       const int h = g * group + it / n_i;
       const int i = i0 + it % n_i;
       mbar_wait(&bar[B_DQ_FULL], it & 1);
+      if (leader) SA_TR(17);
       tc_fence_after();
-#pragma unroll 1
+      uint32_t o[kChunks][32];  // the whole dQ row, so the TMEM columns free up at once
+#pragma unroll
+      for (int ch = 0; ch < kChunks; ch++) SA_TMEM_LD32(t_dpt + lane_off + ch * 32, o[ch]);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&bar[B_DQ_FREE]);
+      if (leader) SA_TR(18);
+      if (p.debug & 1) continue;
+#pragma unroll
       for (int ch = 0; ch < kChunks; ch++) {
-        uint32_t o[32];
-        SA_TMEM_LD32(t_dpt + lane_off + ch * 32, o);
-        tmem_ld_wait();
-        if (ch == kChunks - 1) {
-          tc_fence_before();
-          mbar_arrive(&bar[B_DQ_FREE]);
-        }
-        if (p.debug & 1) continue;
-        const uint32_t buf = stage + (ch & 1) * kPanelBytes;
-        if (ch >= 2) {
-          if (leader) bulk_wait_read<1>();
-          named_bar_sync(1, 128);
-        }
+        const uint32_t buf = sbase + L::kStg + (ch & 1) * kPanelBytes;
+        if (leader) bulk_wait_read<1>();  // the reduce that last read this buffer is done
+        named_bar_sync(1, 128);
 #pragma unroll
         for (int qd = 0; qd < 8; qd++)
-          sts128(buf + sw128_off(row, qd), __float_as_uint(__uint_as_float(o[4 * qd]) * p.scale),
-                 __float_as_uint(__uint_as_float(o[4 * qd + 1]) * p.scale),
-                 __float_as_uint(__uint_as_float(o[4 * qd + 2]) * p.scale),
-                 __float_as_uint(__uint_as_float(o[4 * qd + 3]) * p.scale));
+          sts128(buf + sw128_off(row, qd),
+                 __float_as_uint(__uint_as_float(o[ch][4 * qd]) * p.scale),
+                 __float_as_uint(__uint_as_float(o[ch][4 * qd + 1]) * p.scale),
+                 __float_as_uint(__uint_as_float(o[ch][4 * qd + 2]) * p.scale),
+                 __float_as_uint(__uint_as_float(o[ch][4 * qd + 3]) * p.scale));
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
-          tma_reduce_add_3d(&p.tdq, smem + L::kDS + (ch & 1) * kPanelBytes, 32 * ch, h, 128 * i);
+          tma_reduce_add_3d(&p.tdq, smem + L::kStg + (ch & 1) * kPanelBytes, 32 * ch, h, 128 * i);
           bulk_commit();
         }
       }
-      if (leader) {
-        bulk_wait_read<0>();
-        mbar_arrive(&bar[B_DSS_FREE]);
-      }
+      if (leader) SA_TR(19);
     }
+    if (leader) bulk_wait<0>();
     // ------------------------------------------------------------ dK epilogue
     mbar_wait(&bar[B_KV_DONE], 0);
     tc_fence_after();
-    const uint32_t kst = sbase + L::kDO;  // dO stages are free now
+    const uint32_t kst = sbase + L::kDO;  // dO + dS buffers (contiguous) are free now
 #pragma unroll 1
     for (int ch = 0; ch < kChunks; ch++) {
       uint32_t o[32];
@@ -431,7 +489,29 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   prm.kind = kind;
   const char* dbg = getenv("SA_BWD_DEBUG");
   prm.debug = dbg ? atoi(dbg) : 0;
-  return d == 128 ? launch_bwd_d<128>(prm, st) : launch_bwd_d<64>(prm, st);
+  prm.trace = nullptr;
+  prm.trace_cta = 0;
+  static long long* trace_buf = nullptr;
+  const char* tr = getenv("SA_BWD_TRACE");  // perf experiments: dump one CTA's timeline
+  if (tr) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 16 * 32 * sizeof(long long));
+    cudaMemsetAsync(trace_buf, 0, 16 * 32 * sizeof(long long), st);
+    prm.trace = trace_buf;
+    prm.trace_cta = atoi(tr);
+  }
+  int r = d == 128 ? launch_bwd_d<128>(prm, st) : launch_bwd_d<64>(prm, st);
+  if (tr && r == 0) {
+    long long h[16 * 32];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost);
+    const long long t0 = h[0];
+    for (int it = 0; it < 16; it++) {
+      fprintf(stderr, "it%2d", it);
+      for (int k = 0; k < 23; k++) fprintf(stderr, " %6lld", h[it * 32 + k] ? h[it * 32 + k] - t0 : -1);
+      fprintf(stderr, "\n");
+    }
+  }
+  return r;
 }
 
 }  // namespace sa
