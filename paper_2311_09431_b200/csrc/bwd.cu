@@ -100,8 +100,11 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
   const uint32_t warp = warp_id(), lane = lane_id();
   if (smem + L::kBytes > smem_raw + L::kAlloc) __trap();  // alignment slack exhausted
 
-  const int j = blockIdx.x / p.hkv;  // key tile: small j = most query tiles (LPT first)
-  const int g = blockIdx.x % p.hkv;
+  // Head-major order: the ~148 concurrent CTAs share one kv head, so that head's Q / dO
+  // and its dq_acc rows (the reduce-add target) stay L2-resident.  Within a head, small j
+  // (most query tiles) first (LPT).
+  const int g = blockIdx.x / p.n_t;
+  const int j = blockIdx.x % p.n_t;
   const int group = p.hq / p.hkv;
   const bool causal = p.kind != SA_MASK_FULLY_UNMASKED;
   const int i0 = causal ? j : 0;

@@ -72,8 +72,10 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int b = blockIdx.x;
-  const int qb = p.n_qblk - 1 - b / p.hq;  // heaviest query blocks first (causal LPT)
-  const int h = b % p.hq;
+  // Head-major order keeps the K/V of ~1 head (a few MB) L2-resident while the ~148
+  // concurrent CTAs stream it; within a head the heaviest query blocks go first (LPT).
+  const int h = b / p.n_qblk;
+  const int qb = p.n_qblk - 1 - b % p.n_qblk;
   const int kvh = h / (p.hq / p.hkv);
   const int r0 = qb * 256;
   const bool causal = p.kind != SA_MASK_FULLY_UNMASKED;
