@@ -143,42 +143,50 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t id_s = idesc_bf16(128, 128, 0, 0);
-      const uint32_t id_o = idesc_bf16(128, D, 0, 1);
-      const uint32_t q_addr[2] = {smem_u32(smem + L::kQ0), smem_u32(smem + L::kQ1)};
+    // Whole warp walks the schedule (descriptor words warp-uniform); one elected lane issues.
+    {
+      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t id_o = idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t hi = sdesc_hi(1024);
+      const uint32_t sbase = smem_u32(smem);
       auto issue_s = [&](int t, int s) {
-        const uint32_t k_addr = smem_u32(smem + L::kK + s * L::kTile);
+        if (elect_one()) {
+          const uint32_t a = opaque(sdesc_lo(sbase + (t ? L::kQ1 : L::kQ0), 16));
+          const uint32_t b = opaque(sdesc_lo(sbase + L::kK + s * L::kTile, 16));
 #pragma unroll
-        for (int kk = 0; kk < kKSteps; kk++) {
-          const uint32_t off = (kk >> 2) * kPanelBytes + (kk & 3) * 32;
-          mma_ss(tbase + t * 128, sdesc(q_addr[t] + off, 16, 1024), sdesc(k_addr + off, 16, 1024),
-                 id_s, kk > 0);
+          for (int kk = 0; kk < kKSteps; kk++) {
+            const uint32_t off = ((kk >> 2) * kPanelBytes + (kk & 3) * 32) >> 4;
+            mma_ss2(tbase + t * 128, a + off, hi, b + off, hi, id_s, kk > 0);
+          }
+          mma_commit(&s_full[t]);
         }
-        mma_commit(&s_full[t]);
+        __syncwarp();
       };
       mbar_wait(&q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       for (int t = 0; t < 2; t++)
         if (n_t[t] > 0) issue_s(t, 0);
-      mma_commit(&k_empty[0]);
+      if (elect_one()) mma_commit(&k_empty[0]);
+      __syncwarp();
       for (int j = 0; j < n_cta; j++) {
         const int sv = j % kStages;
         mbar_wait(&v_full[sv], (j / kStages) & 1);
-        const uint32_t v_addr = smem_u32(smem + L::kV + sv * L::kTile);
         bool k_next = false;
         const int sk = (j + 1) % kStages;
         for (int t = 0; t < 2; t++) {
           if (j < n_t[t]) {
             mbar_wait(&p_full[t], j & 1);
             tc_fence_after();
-            const uint32_t o_t = tbase + 256 + t * D;
+            if (elect_one()) {
+              const uint32_t b = opaque(sdesc_lo(sbase + L::kV + sv * L::kTile, kPanelBytes));
 #pragma unroll
-            for (int kk = 0; kk < 8; kk++)
-              mma_ts(o_t, tbase + t * 128 + kk * 8, sdesc(v_addr + kk * 2048, kPanelBytes, 1024),
-                     id_o, (j > 0 || kk > 0) ? 1u : 0u);
-            mma_commit(&o_done[t]);
+              for (int kk = 0; kk < 8; kk++)
+                mma_ts2(tbase + 256 + t * D, tbase + t * 128 + kk * 8, b + kk * 128, hi, id_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+              mma_commit(&o_done[t]);
+            }
+            __syncwarp();
           }
           if (j + 1 < n_t[t]) {
             if (!k_next) {
@@ -189,10 +197,13 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
             issue_s(t, sk);
           }
         }
-        mma_commit(&v_empty[sv]);
-        if (k_next) mma_commit(&k_empty[sk]);
+        if (elect_one()) {
+          mma_commit(&v_empty[sv]);
+          if (k_next) mma_commit(&k_empty[sk]);
+        }
+        __syncwarp();
       }
-      if (p.tiles) atomicAdd(p.tiles, (unsigned long long)(n_t[0] + n_t[1]));
+      if (p.tiles && lane == 0) atomicAdd(p.tiles, (unsigned long long)(n_t[0] + n_t[1]));
     }
    }
   } else {
@@ -221,9 +232,14 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
         for (int i = 0; i < 128; i++)
           if (!allowed(p.kind, x, j * 128 + i, p.c)) r[i] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      // 8 independent partial maxima / sums: no 128-long dependency chains
+      float mx8[8];
 #pragma unroll
-      for (int i = 0; i < 128; i++) mx = fmaxf(mx, __uint_as_float(r[i]));
+      for (int u = 0; u < 8; u++) mx8[u] = __uint_as_float(r[u]);
+#pragma unroll
+      for (int i = 8; i < 128; i++) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(r[i]));
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float mt = mx * p.scale_log2;
       float factor = 1.f;
       bool resc = false;
@@ -235,14 +251,16 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
         resc = true;
       }
       const float m_use = (m == -INFINITY) ? 0.f : m;
-      float sum = 0.f;
+      float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int i = 0; i < 64; i++) {
         const float p0 = ex2(fmaf(__uint_as_float(r[2 * i]), p.scale_log2, -m_use));
         const float p1 = ex2(fmaf(__uint_as_float(r[2 * i + 1]), p.scale_log2, -m_use));
-        sum += p0 + p1;
+        s8[(2 * i) & 7] += p0;
+        s8[(2 * i + 1) & 7] += p1;
         r[i] = pack_bf16(p0, p1);
       }
+      const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
       l = l * factor + sum;
       SA_TMEM_ST32(t_s + 0, (r + 0));
       SA_TMEM_ST32(t_s + 32, (r + 32));
