@@ -258,6 +258,48 @@ SA_DEV float ex2(float x) {
   return y;
 }
 
+// ---- packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2: two lanes' worth per issue)
+SA_DEV void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n\t.reg .b64 a, b, c, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+      "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+SA_DEV void add2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+SA_DEV void mul2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\t"
+      "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// 2^x for a pair on the FMA pipe (offloads the MUFU unit, which alone caps the softmax):
+// round-to-nearest split x = j + f with the 1.5*2^23 trick, f in [-0.5, 0.5], degree-3
+// polynomial (max rel. error 7.7e-5, far below the bf16 rounding P gets next), exponent
+// added as an integer.  Valid for x in [-125, 126]; smaller x clamps to 2^-125.
+SA_DEV void ex2_poly2(float& y0, float& y1, float x0, float x1) {
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23
+  x0 = fmaxf(x0, -125.f);
+  x1 = fmaxf(x1, -125.f);
+  float t0, t1, r0, r1, f0, f1, p0, p1;
+  add2(t0, t1, x0, x1, kMagic, kMagic);
+  add2(r0, r1, t0, t1, -kMagic, -kMagic);
+  add2(f0, f1, x0, x1, -r0, -r1);
+  fma2(p0, p1, f0, f1, 0.05509095639f, 0.05509095639f, 0.2426045388f, 0.2426045388f);
+  fma2(p0, p1, p0, p1, f0, f1, 0.6932758689f, 0.6932758689f);
+  fma2(p0, p1, p0, p1, f0, f1, 0.9999288917f, 0.9999288917f);
+  y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+  y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 // Byte offset of 16-byte chunk `chunk` (0..7) of row `row` inside a SW128 panel.
 SA_DEV uint32_t sw128_off(uint32_t row, uint32_t chunk) {
   return row * 128u + ((chunk ^ (row & 7u)) << 4);

@@ -25,6 +25,10 @@
 #include "common.cuh"
 #include "internal.h"
 
+#include <cstdio>
+#include <type_traits>
+#include <cstdlib>
+
 namespace sa {
 namespace {
 
@@ -42,7 +46,14 @@ struct FwdParams {
   int c, hq, hkv, n_qblk;
   float scale_log2;
   int kind, first, last;
+  long long* trace;  // perf experiments only: per-iteration clock64 stamps of one CTA
+  int trace_cta;
 };
+
+#define SA_TR(slot)                                                                     \
+  do {                                                                                  \
+    if (p.trace && blockIdx.x == p.trace_cta && j < 16) p.trace[j * 32 + (slot)] = clock64(); \
+  } while (0)
 
 template <int D>
 struct FwdSmem {
@@ -130,11 +141,13 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
         const int s = j % kStages;
         const uint32_t ph = (j / kStages) & 1;
         if (j >= kStages) mbar_wait(&k_empty[s], ph ^ 1);
+        SA_TR(12);
         mbar_arrive_expect_tx(&k_full[s], L::kTile);
         for (int pn = 0; pn < kPanels; pn++)
           tma_load_3d(smem + L::kK + s * L::kTile + pn * kPanelBytes, &p.tk, &k_full[s], 64 * pn,
                       kvh, 128 * j, pol_kv);
         if (j >= kStages) mbar_wait(&v_empty[s], ph ^ 1);
+        SA_TR(13);
         mbar_arrive_expect_tx(&v_full[s], L::kTile);
         for (int pn = 0; pn < kPanels; pn++)
           tma_load_3d(smem + L::kV + s * L::kTile + pn * kPanelBytes, &p.tv, &v_full[s], 64 * pn,
@@ -177,6 +190,7 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
         for (int t = 0; t < 2; t++) {
           if (j < n_t[t]) {
             mbar_wait(&p_full[t], j & 1);
+            SA_TR(t ? 3 : 0);
             tc_fence_after();
             if (elect_one()) {
               const uint32_t b = opaque(sdesc_lo(sbase + L::kV + sv * L::kTile, kPanelBytes));
@@ -187,6 +201,7 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
               mma_commit(&o_done[t]);
             }
             __syncwarp();
+            SA_TR(t ? 4 : 1);
           }
           if (j + 1 < n_t[t]) {
             if (!k_next) {
@@ -195,6 +210,7 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
               k_next = true;
             }
             issue_s(t, sk);
+            SA_TR(t ? 5 : 2);
           }
         }
         if (elect_one()) {
@@ -219,6 +235,7 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n; j++) {
       mbar_wait(&s_full[t], j & 1);
+      if (lane == 0 && (warp & 3) == 0) SA_TR(t ? 10 : 8);
       tc_fence_after();
       uint32_t r[128];
       SA_TMEM_LD32(t_s + 0, (r + 0));
@@ -226,41 +243,64 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
       SA_TMEM_LD32(t_s + 64, (r + 64));
       SA_TMEM_LD32(t_s + 96, (r + 96));
       tmem_ld_wait();
+      // Diagonal / ragged tile: key columns >= lim are masked (y <= x, y < x, y < c).
       const bool masked = (causal && j == (qb * 2 + t)) || (j + 1) * 128 > p.c;
-      if (masked) {
-#pragma unroll
-        for (int i = 0; i < 128; i++)
-          if (!allowed(p.kind, x, j * 128 + i, p.c)) r[i] = __float_as_uint(-INFINITY);
-      }
-      // 8 independent partial maxima / sums: no 128-long dependency chains
-      float mx8[8];
-#pragma unroll
-      for (int u = 0; u < 8; u++) mx8[u] = __uint_as_float(r[u]);
-#pragma unroll
-      for (int i = 8; i < 128; i++) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(r[i]));
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float mt = mx * p.scale_log2;
       float factor = 1.f;
       bool resc = false;
-      if (m == -INFINITY) {
-        m = mt;
-      } else if (mt > m + kRescaleThreshold) {
-        factor = ex2(m - mt);
-        m = mt;
-        resc = true;
-      }
-      const float m_use = (m == -INFINITY) ? 0.f : m;
-      float s8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // Two instantiations so the common (unmasked) tile carries no per-element selects.
+      auto tile = [&](auto masked_tag) {
+        constexpr bool kMasked = decltype(masked_tag)::value;
+        int lim = 128;
+        if constexpr (kMasked) {
+          const int last = p.kind == SA_MASK_CAUSAL_INCLUSIVE   ? x + 1
+                           : p.kind == SA_MASK_CAUSAL_EXCLUSIVE ? x
+                                                                : p.c;
+          lim = min(last, p.c) - j * 128;
 #pragma unroll
-      for (int i = 0; i < 64; i++) {
-        const float p0 = ex2(fmaf(__uint_as_float(r[2 * i]), p.scale_log2, -m_use));
-        const float p1 = ex2(fmaf(__uint_as_float(r[2 * i + 1]), p.scale_log2, -m_use));
-        s8[(2 * i) & 7] += p0;
-        s8[(2 * i + 1) & 7] += p1;
-        r[i] = pack_bf16(p0, p1);
-      }
-      const float sum = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
+          for (int i = 0; i < 128; i++)
+            if (i >= lim) r[i] = __float_as_uint(-INFINITY);
+        }
+        // 8 independent partial maxima: no 128-long dependency chain
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) mx8[u] = __uint_as_float(r[u]);
+#pragma unroll
+        for (int i = 8; i < 128; i++) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(r[i]));
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const float mt = mx * p.scale_log2;
+        if (m == -INFINITY) {
+          m = mt;
+        } else if (mt > m + kRescaleThreshold) {
+          factor = ex2(m - mt);
+          m = mt;
+          resc = true;
+        }
+        const float neg_m = (m == -INFINITY) ? 0.f : -m;
+        // p = 2^(s*scale*log2e - m): pairs through FFMA2; 7 of every 16 pairs take the
+        // FMA-pipe polynomial, the rest MUFU.EX2 (balances the two pipes); 4 FADD2 chains.
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 64; i++) {
+          float x0, x1, p0, p1;
+          fma2(x0, x1, __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), p.scale_log2,
+               p.scale_log2, neg_m, neg_m);
+          if ((i & 15) < 7) {
+            ex2_poly2(p0, p1, x0, x1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          if constexpr (kMasked) {
+            p0 = 2 * i < lim ? p0 : 0.f;
+            p1 = 2 * i + 1 < lim ? p1 : 0.f;
+          }
+          add2(sa[i & 3], sb[i & 3], sa[i & 3], sb[i & 3], p0, p1);
+          r[i] = pack_bf16(p0, p1);
+        }
+        return ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sb[0] + sb[1]) + (sb[2] + sb[3]));
+      };
+      const float sum = masked ? tile(std::true_type{}) : tile(std::false_type{});
       l = l * factor + sum;
       SA_TMEM_ST32(t_s + 0, (r + 0));
       SA_TMEM_ST32(t_s + 32, (r + 32));
@@ -280,6 +320,7 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&p_full[t]);
+      if (lane == 0 && (warp & 3) == 0) SA_TR(t ? 11 : 9);
     }
     if (n > 0) {
       // -------------------------------------------------------- epilogue + LSE merge
@@ -383,6 +424,30 @@ int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float*
   prm.kind = kind;
   prm.first = first;
   prm.last = last;
+  prm.trace = nullptr;
+  prm.trace_cta = 0;
+  static long long* trace_buf = nullptr;
+  const char* tr = getenv("SA_FWD_TRACE");  // perf experiments: dump one CTA's timeline
+  if (tr) {
+    if (!trace_buf) cudaMalloc(&trace_buf, 16 * 32 * sizeof(long long));
+    cudaMemsetAsync(trace_buf, 0, 16 * 32 * sizeof(long long), st);
+    prm.trace = trace_buf;
+    prm.trace_cta = atoi(tr);
+  }
+  if (tr) {
+    int r = d == 128 ? launch_fwd_d<128>(prm, st) : launch_fwd_d<64>(prm, st);
+    long long hbuf[16 * 32];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(hbuf, trace_buf, sizeof hbuf, cudaMemcpyDeviceToHost);
+    const long long t0 = hbuf[12];
+    for (int jj = 0; jj < 16; jj++) {
+      fprintf(stderr, "j%2d", jj);
+      for (int k = 0; k < 14; k++)
+        fprintf(stderr, " %6lld", hbuf[jj * 32 + k] ? hbuf[jj * 32 + k] - t0 : -1);
+      fprintf(stderr, "\n");
+    }
+    return r;
+  }
   return d == 128 ? launch_fwd_d<128>(prm, st) : launch_fwd_d<64>(prm, st);
 }
 
