@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstriped_attn.so")
+LIB_PATH = os.environ.get("SA_LIB_PATH") or os.path.join(_HERE, "libstriped_attn.so")
 
 _lib = None
 
