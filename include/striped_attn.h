@@ -97,6 +97,12 @@ int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, 
 /* dst_bf16[i] = bf16(src[i]) (finalises dq/dk/dv accumulators and skipped last steps). */
 int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
 
+/* Strided host<->device row copy (cudaMemcpy2DAsync): `height` rows of `width` bytes,
+ * row pitches in bytes.  Used by the host-streaming API to move one head group of a
+ * token-major [c, H, D] tensor without a host-side gather. */
+int sa_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                      int64_t height, void* stream);
+
 /* Test-only: exercises the tcgen05 / TMA operand layouts the kernels rely on, on one
  * 128x128x128 tile: s = a b^T, o = bf16(s) v, y = b^T v (a, b, v bf16 [128,128] row-major;
  * outputs fp32 [128,128]). */

@@ -174,6 +174,21 @@ int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream) {
   return launch_cast(src, dst, n, static_cast<cudaStream_t>(stream));
 }
 
+int sa_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                      int64_t height, void* stream) {
+  if (!dst || !src || width < 0 || height < 0 || dpitch < width || spitch < width)
+    return fail_arg("bad 2-D copy arguments");
+  if (width == 0 || height == 0) return 0;
+  cudaError_t e = cudaMemcpy2DAsync(dst, (size_t)dpitch, src, (size_t)spitch, (size_t)width,
+                                    (size_t)height, cudaMemcpyDefault,
+                                    static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMemcpy2DAsync: ") + cudaGetErrorString(e));
+    return -static_cast<int>(e);
+  }
+  return 0;
+}
+
 int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* o, float* y,
                   void* stream) {
   if (!a || !b || !v || !s || !o || !y) return fail_arg("null pointer");
