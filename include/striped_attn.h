@@ -109,6 +109,11 @@ int sa_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch
 int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* o, float* y,
                   void* stream);
 
+/* Test-only: the CTA-pair (tcgen05 cta_group::2) operand layouts: s = a b^T (a [256,128],
+ * b [128,128]), o = bf16(s) v (v [128,128]), s2 = a b^T with A staged in TMEM. */
+int sa_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

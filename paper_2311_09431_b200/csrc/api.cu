@@ -195,4 +195,10 @@ int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* 
   return launch_probe(a, b, v, s, o, y, static_cast<cudaStream_t>(stream));
 }
 
+int sa_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
+                  void* stream) {
+  if (!a || !b || !v || !s || !o || !s2) return fail_arg("null pointer");
+  return launch_probe_pair(a, b, v, s, o, s2, static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

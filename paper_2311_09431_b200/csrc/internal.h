@@ -26,6 +26,8 @@ int launch_permute(const void* src, void* dst, int64_t n_seq, int32_t n_dev, int
                    int32_t scheme, int32_t direction, int32_t device, cudaStream_t st);
 int launch_probe(const void* a, const void* b, const void* v, float* s, float* o, float* y,
                  cudaStream_t st);
+int launch_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
+                      cudaStream_t st);
 int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float* lse, void* out,
                int64_t c, int32_t hq, int32_t hkv, int32_t d, float scale, int32_t kind,
                int32_t first, int32_t last, int64_t* tiles, cudaStream_t st);

@@ -28,6 +28,20 @@ def test_umma_probe_layouts(ops):
     assert (y - y_ref).abs().max().item() < 1e-3
 
 
+def test_umma_pair_probe_layouts(ops):
+    """cta_group::2: A rows split over the CTA pair, B split by N, P and A staged in TMEM."""
+    g = torch.Generator(device="cuda").manual_seed(1)
+    a = torch.randn(256, 128, device="cuda", generator=g).bfloat16()
+    b = torch.randn(128, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(128, 128, device="cuda", generator=g).bfloat16()
+    s, o, s2 = ops.probe_pair(a, b, v)
+    torch.cuda.synchronize()
+    s_ref = a.float() @ b.float().T
+    assert (s - s_ref).abs().max().item() < 1e-3
+    assert (o - s.bfloat16().float() @ v.float()).abs().max().item() < 1e-2
+    assert (s2 - s_ref).abs().max().item() < 1e-3
+
+
 @pytest.mark.parametrize("scheme", [0, 1])
 @pytest.mark.parametrize("n_dev,n_seq,heads,d", [(4, 64, 2, 128), (8, 4096, 4, 64), (3, 12, 1, 64),
                                                  (2, 6, 3, 2)])
