@@ -274,9 +274,11 @@ SA_DEV uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// Arrive on a (possibly remote) barrier of the cluster.  Default .release.cta semantics:
+// .release.cluster costs ~1000 clk per arrive on sm_100 and is not needed for the
+// tcgen05 hand-off (tcgen05.wait::st + fence::before_thread_sync order the TMEM writes).
 SA_DEV void mbar_arrive_cluster(uint32_t cluster_saddr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_saddr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_saddr) : "memory");
 }
 template <uint32_t kCols>
 SA_DEV void tmem_alloc2(uint32_t* dst_smem) {  // one warp in EACH CTA of the pair
@@ -390,6 +392,11 @@ SA_DEV float4 lds128f(uint32_t saddr) {
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "r"(saddr)
                : "memory");
+  return v;
+}
+SA_DEV float lds32f(uint32_t saddr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(saddr) : "memory");
   return v;
 }
 SA_DEV void sts32f(uint32_t saddr, float v) {

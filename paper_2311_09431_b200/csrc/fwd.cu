@@ -411,6 +411,8 @@ int launch_fwd_d(FwdParams& prm, cudaStream_t st) {
 int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float* lse, void* out,
                int64_t c, int32_t hq, int32_t hkv, int32_t d, float scale, int32_t kind,
                int32_t first, int32_t last, int64_t* tiles, cudaStream_t st) {
+  if (fwd_pair_enabled(d) && !getenv("SA_FWD_TRACE"))
+    return launch_fwd_pair(q, k, v, o_acc, lse, out, c, hq, hkv, scale, kind, first, last, tiles, st);
   FwdParams prm;
   if (int r = make_tmap_rows(&prm.tq, q, c, hq, d, 128)) return r;
   if (int r = make_tmap_rows(&prm.tk, k, c, hkv, d, 128)) return r;

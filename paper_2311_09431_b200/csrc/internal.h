@@ -28,6 +28,10 @@ int launch_probe(const void* a, const void* b, const void* v, float* s, float* o
                  cudaStream_t st);
 int launch_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
                       cudaStream_t st);
+bool fwd_pair_enabled(int32_t d);
+int launch_fwd_pair(const void* q, const void* k, const void* v, float* o_acc, float* lse,
+                    void* out, int64_t c, int32_t hq, int32_t hkv, float scale, int32_t kind,
+                    int32_t first, int32_t last, int64_t* tiles, cudaStream_t st);
 int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float* lse, void* out,
                int64_t c, int32_t hq, int32_t hkv, int32_t d, float scale, int32_t kind,
                int32_t first, int32_t last, int64_t* tiles, cudaStream_t st);
