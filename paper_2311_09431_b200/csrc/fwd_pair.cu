@@ -53,7 +53,7 @@ constexpr float kRescaleThreshold = 8.0f;
 #define SA_PROD_WARP 0
 #endif
 #ifndef SA_FWD_POLY
-#define SA_FWD_POLY 4
+#define SA_FWD_POLY 2
 #endif
 
 struct PairParams {

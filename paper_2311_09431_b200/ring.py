@@ -111,6 +111,34 @@ class _Streams:
             self.compute.wait_stream(self.comm)
 
 
+class _StepTimer:
+    """CUDA-event time of each round's block kernel on the compute stream (telemetry)."""
+
+    def __init__(self, ref: torch.Tensor, enabled: bool):
+        self.on = enabled and _is_cuda(ref)
+        self.events = []
+
+    def start(self):
+        if self.on:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.events.append([e, None])
+
+    def stop(self):
+        if self.on:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.events[-1][1] = e
+
+    def fill(self, records):
+        """Write the measured ms into the last len(events) StepRecords."""
+        if not self.on or not self.events:
+            return
+        self.events[-1][1].synchronize()
+        for rec, (a, b) in zip(records[-len(self.events):], self.events):
+            rec.compute_ms = a.elapsed_time(b)
+
+
 def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale: float,
                  block_ops: BlockOps | None = None, stats: RingStats | None = None,
                  count_tiles: bool = False):
@@ -126,12 +154,16 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
     lse = torch.empty(hq, c, device=q.device, dtype=torch.float32)
     o_acc = None if world == 1 else torch.empty(c, hq, d, device=q.device, dtype=torch.float32)
     tiles = torch.zeros(1, device=q.device, dtype=torch.int64) if count_tiles else None
+    timer = _StepTimer(q, stats is not None)
     if world == 1:
         kind = masks.block_mask(layout, 0, 0, 1)
+        timer.start()
         bops.fwd_block(q, k, v, None, lse, out, softmax_scale, kind, True, True, tiles)
+        timer.stop()
         if stats is not None:
             stats.rounds.append(StepRecord(0, 0, int(kind),
                                            int(tiles.item()) if tiles is not None else 0))
+            timer.fill(stats.rounds)
         return out, lse
     comm = _Comm(group)
     st = _Streams(q)
@@ -147,8 +179,10 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
                 pending = comm.exchange(list(cur), list(nxt))
         kind = masks.block_mask(layout, rank, held, world)
         before = int(tiles.item()) if (tiles is not None and stats is not None) else 0
+        timer.start()
         bops.fwd_block(q, cur[0], cur[1], o_acc, lse, out, softmax_scale, kind, i == 0,
                        i == world - 1, tiles)
+        timer.stop()
         if stats is not None:
             after = int(tiles.item()) if tiles is not None else 0
             stats.rounds.append(StepRecord(i, held, int(kind), after - before))
@@ -158,11 +192,14 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
                     w.wait()
             st.compute_after_comm()
             cur = nxt
+    if stats is not None:
+        timer.fill(stats.rounds)
     return out, lse
 
 
 def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped",
-                  softmax_scale: float, block_ops: BlockOps | None = None):
+                  softmax_scale: float, block_ops: BlockOps | None = None,
+                  stats: RingStats | None = None):
     """Backward for this rank's stripe -> (dq, dk, dv) bf16 in local order.
 
     K/V hop one rank per round (prefetched on the side stream); the fp32 dK/dV
@@ -179,9 +216,14 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
     bops.bwd_preprocess(out, dout, dsum, dq_acc)
     dk_acc = torch.zeros(c, hkv, d, device=dev, dtype=torch.float32)
     dv_acc = torch.zeros(c, hkv, d, device=dev, dtype=torch.float32)
+    timer = _StepTimer(q, stats is not None)
     if world == 1:
         kind = masks.block_mask(layout, 0, 0, 1)
+        timer.start()
         bops.bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale, kind)
+        timer.stop()
+        if stats is not None:
+            stats.rounds.append(StepRecord(0, 0, int(kind)))
     else:
         comm = _Comm(group)
         st = _Streams(q)
@@ -199,8 +241,12 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
                 with st.on_comm():
                     pending = comm.exchange(list(cur), list(nxt))
             kind = masks.block_mask(layout, rank, held, world)
+            timer.start()
             bops.bwd_block(q, cur[0], cur[1], dout, lse, dsum, dq_acc, dcur[0], dcur[1],
                            softmax_scale, kind)
+            timer.stop()
+            if stats is not None:
+                stats.rounds.append(StepRecord(i, held, int(kind)))
             # dK/dV of the held stripe move on after this round's compute (N hops total)
             st.comm_after_compute()
             with st.on_comm():
@@ -215,6 +261,8 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
             if pending is not None:
                 cur = nxt
         dk_acc, dv_acc = dcur
+    if stats is not None:
+        timer.fill(stats.rounds)
     dq = torch.empty_like(q)
     dk = torch.empty_like(k)
     dv = torch.empty_like(v)

@@ -22,6 +22,9 @@ class OracleBlockOps:
     def fwd_block(self, q, k, v, o_acc, lse, out, scale, kind, first, last, tiles=None):
         self.calls.append(("fwd", int(kind), bool(first), bool(last)))
         c, hq, d = q.shape
+        if tiles is not None and c % 128 == 0:  # what the kernel's counter reports
+            cen = R.tile_census(int(kind), c, c, 128, 128)
+            tiles += hq * (cen.n_full + cen.n_partial)
         if kind == R.FULLY_MASKED:
             o_blk = np.zeros((c, hq, d))
             l_blk = np.full((hq, c), -np.inf)

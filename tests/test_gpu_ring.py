@@ -245,3 +245,31 @@ def test_host_streaming_api_matches_device_api(pkg, groups):
     assert torch.equal(dk, dk_ref.cpu()) and torch.equal(dv, dv_ref.cpu())
     # dQ partials are reduce-added by many CTAs in hardware order: equal up to fp32 order
     assert (dq.float() - dq_ref.cpu().float()).abs().max().item() <= 1e-2
+
+
+@pytest.mark.parametrize("layout,scheme", [("striped", R.STRIPED), ("ring", R.CONTIGUOUS)])
+def test_kernel_tile_counts_match_reference_schedule(pkg, layout, scheme):
+    """the kernels' own tile counters, per (rank, round), equal heads x the
+    reference's schedule_work_stats census (simulator.py:280-315) at 128 x 128 tiles, and
+    the telemetry rows reproduce the reference CSV columns."""
+    from paper_2311_09431_b200 import ring, telemetry
+    n_dev, c, hq, d = 4, 1024, 4, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    mk = lambda: [torch.randn(c, hq, d, device="cuda", generator=g).bfloat16() for _ in range(n_dev)]
+    qs, ks, vs = mk(), mk(), mk()
+    _, _, stats = ring.virtual_ring_forward(qs, ks, vs, layout=layout, softmax_scale=d ** -0.5,
+                                            count_tiles=True)
+    run = telemetry.Run(layout, c, hq, stats)
+    assert telemetry.check_tile_counts(run) == []
+    want = R.schedule_work_stats(scheme, n_dev, c, 128, 128)
+    for row in telemetry.rows([run]):
+        rs = want[row[2]].rounds[row[1]]
+        assert row[3:] == [rs.block_index, rs.tiles_total, rs.tiles_skipped, rs.tiles_partial,
+                           rs.tiles_full, rs.interactions_computed, rs.interactions_required]
+    # single-rank ring_forward records the kernel's CUDA-event time
+    st = ring.RingStats(0)
+    ring.ring_forward(qs[0], ks[0], vs[0], layout=layout, softmax_scale=d ** -0.5, stats=st,
+                      count_tiles=True)
+    assert len(st.rounds) == 1 and st.rounds[0].compute_ms > 0
+    assert st.rounds[0].tiles_computed == hq * R.tile_census(R.CAUSAL_INCLUSIVE, c, c, 128, 128).n_full \
+        + hq * R.tile_census(R.CAUSAL_INCLUSIVE, c, c, 128, 128).n_partial

@@ -1,6 +1,8 @@
 """CPU tests of the product's host logic and the C-ABI library surface (no GPU needed)."""
 
 import ctypes
+
+import numpy as np
 import os
 import re
 
@@ -124,3 +126,43 @@ def test_product_never_imports_the_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), f
                 assert "oracle/" not in src.replace("oracle/ ", ""), f
+
+
+def test_telemetry_csv_matches_reference_schema_and_oracle(tmp_path):
+    """Rows of a (virtual, oracle-backed) ring run in the reference CSV schema
+    (cli.py:38-49) equal the oracle's schedule_work_stats (simulator.py:280-315) at the
+    kernel's 128 x 128 tiles; the kernel-counted tiles pass the census check."""
+    import csv as _csv
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from cpu_blockops import OracleBlockOps
+    from paper_2311_09431_b200 import ring, telemetry
+
+    n_dev, c, hq, d = 4, 256, 2, 8
+    rng = np.random.default_rng(3)
+    for layout, scheme in (("striped", R.STRIPED), ("ring", R.CONTIGUOUS)):
+        qs, ks, vs = ([torch.tensor(rng.standard_normal((c, hq, d))) for _ in range(n_dev)]
+                      for _ in range(3))
+        _, _, stats = ring.virtual_ring_forward(qs, ks, vs, layout=layout, softmax_scale=0.2,
+                                                block_ops=OracleBlockOps(), count_tiles=True)
+        run = telemetry.Run(layout, c, hq, stats)
+        assert telemetry.check_tile_counts(run) == []
+        path = tmp_path / f"{layout}.csv"
+        telemetry.write_stats_csv(str(path), [run], extra=True)
+        with open(path, encoding="utf-8") as fh:
+            table = list(_csv.reader(fh))
+        assert table[0] == telemetry.STATS_CSV_HEADER + telemetry.EXTRA_COLUMNS
+        want = R.schedule_work_stats(scheme, n_dev, c, 128, 128)
+        body = table[1:]
+        assert len(body) == n_dev * n_dev
+        for row in body:
+            i, dev = int(row[1]), int(row[2])
+            rs = want[dev].rounds[i]
+            assert [int(x) for x in row[3:10]] == [rs.block_index, rs.tiles_total, rs.tiles_skipped,
+                                                   rs.tiles_partial, rs.tiles_full,
+                                                   rs.interactions_computed,
+                                                   rs.interactions_required]
+            assert int(row[11]) == hq * (rs.tiles_full + rs.tiles_partial)
+        # a wrong count is reported
+        stats[0].rounds[0].tiles_computed += 1
+        assert len(telemetry.check_tile_counts(run)) == 1

@@ -36,7 +36,7 @@ def _worker(rank, world, port, layout, result_q):
         sys.path.insert(0, here)
         sys.path.insert(0, os.path.dirname(here))
         from cpu_blockops import OracleBlockOps
-        from paper_2311_09431_b200 import ring
+        from paper_2311_09431_b200 import ring, telemetry
 
         n, hq, hkv, d = 16 * world, 4, 2, 8
         rng = np.random.default_rng(7)
@@ -62,7 +62,12 @@ def _worker(rank, world, port, layout, result_q):
         }
         held = [r.block_index for r in stats.rounds]
         kinds = [r.mask_kind for r in stats.rounds]
-        result_q.put((rank, errs, held, kinds, ops.calls))
+        # telemetry: every rank's stats on every rank, rows in the reference CSV schema
+        everyone = telemetry.gather_stats(stats)
+        run = telemetry.Run(layout, n // world, hq, everyone)
+        csv_rows = telemetry.rows([run])
+        imb = telemetry.step_imbalance(everyone)
+        result_q.put((rank, errs, held, kinds, ops.calls, csv_rows, imb))
     finally:
         dist.destroy_process_group()
 
@@ -80,7 +85,15 @@ def test_ring_driver_over_gloo(world, layout):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for rank, errs, held, kinds, calls in results:
+    rows0 = None
+    for rank, errs, held, kinds, calls, csv_rows, imb in results:
+        # every rank gathered the same table: world rounds x world devices, round-major
+        assert len(csv_rows) == world * world
+        assert [(r[1], r[2]) for r in csv_rows] == [(i, d) for i in range(world) for d in range(world)]
+        assert all(r[3] == (r[2] - r[1]) % world for r in csv_rows)  # held = (j - i) mod N
+        assert rows0 is None or csv_rows == rows0
+        rows0 = csv_rows
+        assert imb == [1.0] * world  # no CUDA timing on CPU
         for name, e in errs.items():
             assert e <= 1e-5, (rank, name, e)  # lse/out carried in fp32 by the driver
         assert held == [(rank - i) % world for i in range(world)]
