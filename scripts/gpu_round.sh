@@ -19,6 +19,6 @@ fi
 if [ "${NCU_FULL:-0}" = "1" ]; then
   CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu"
   timeout 300 $CMD > gpurun_out/plain_full.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"bwd_kernel|fwd_kernel" \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"bwd_kernel|fwd_pair_kernel|fwd_kernel" \
       -s 2 -c 2 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
