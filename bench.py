@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--dim", type=int, default=128)
     ap.add_argument("--stripe", type=int, default=STRIPE, help="tokens per rank")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--head-groups", type=int, default=8,
+                    help="e2e: head groups streamed by the host API (copy/compute overlap); "
+                         "0 = host.ramp_groups (small first/last groups)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ring-compare", action="store_true")
     return ap.parse_args()
@@ -324,14 +327,19 @@ def main():
     # timed region (overlapped with compute across head groups by the API itself).
     e2e = None
     if not args.no_e2e:
-        from paper_2311_09431_b200.host import attention_fwd_bwd_host
+        from paper_2311_09431_b200.host import attention_fwd_bwd_host, ramp_groups
         hq_h, hk_h, hv_h, hdo_h = (x.cpu().pin_memory() for x in (q, k, v, dout))
         hout = torch.empty(c, hq, d, dtype=torch.bfloat16).pin_memory()
         hdq = torch.empty(c, hq, d, dtype=torch.bfloat16).pin_memory()
         hdk = torch.empty(c, hkv, d, dtype=torch.bfloat16).pin_memory()
         hdv = torch.empty(c, hkv, d, dtype=torch.bfloat16).pin_memory()
         hlse = torch.empty(hq, c, dtype=torch.float32).pin_memory()
-        groups = 4 if hq % 4 == 0 and hkv % 4 == 0 else 1
+        if args.head_groups > 0:
+            groups = args.head_groups
+            while groups > 1 and (hq % groups or hkv % groups):
+                groups //= 2
+        else:
+            groups = ramp_groups(hq, hkv)
 
         def e2e_step():
             ev = attention_fwd_bwd_host(hq_h, hk_h, hv_h, hdo_h, hout, hlse, hdq, hdk, hdv,

@@ -41,41 +41,73 @@ def _copy2d(dst: torch.Tensor, src: torch.Tensor, heads: slice, to_device: bool,
                                                 width, c, stream.cuda_stream), "sa_memcpy2d_async")
 
 
+def ramp_groups(hq: int, hkv: int, max_groups: int = 16) -> list:
+    """Head-group sizes (q heads) for streaming: small groups first and last, so only a
+    small H2D before the first kernel and a small D2H after the last one are exposed,
+    large groups in the middle.  Every size is a multiple of Hq/Hkv (whole kv heads)."""
+    r = hq // hkv
+    units = hkv  # in kv heads
+    lo, hi, step = [], [], 1
+    while units >= 2 * step and len(lo) + len(hi) + 2 <= max_groups:
+        lo.append(step)
+        hi.append(step)
+        units -= 2 * step
+        step *= 2
+    if units:
+        if lo:
+            lo[-1] += units
+        else:
+            lo = [units]
+    sizes = lo + hi[::-1]
+    return [x * r for x in sizes]
+
+
 def attention_fwd_bwd_host(q, k, v, dout, out, lse, dq, dk, dv, *, group=None,
-                           layout: str = "striped", softmax_scale=None, head_groups: int = 4,
+                           layout: str = "striped", softmax_scale=None, head_groups=4,
                            device=None):
     """Forward + backward of this rank's stripe from/to pinned host memory.
 
     q, dout, out, dq: [c, Hq, D] bf16 pinned; k, v, dk, dv: [c, Hkv, D] bf16 pinned;
-    lse: [Hq, c] fp32 pinned.  Returns an event recorded when every result is in host
-    memory (the caller synchronises on it)."""
+    lse: [Hq, c] fp32 pinned.  ``head_groups``: an int (equal groups) or a list of q-head
+    counts per group (each a multiple of Hq/Hkv, summing to Hq; see ``ramp_groups``).
+    Returns an event recorded when every result is in host memory (the caller
+    synchronises on it)."""
     for name, t in (("q", q), ("k", k), ("v", v), ("dout", dout), ("out", out), ("dq", dq),
                     ("dk", dk), ("dv", dv), ("lse", lse)):
         if t.is_cuda or not t.is_pinned() or not t.is_contiguous():
             raise ValueError(f"{name} must be a contiguous pinned host tensor")
     c, hq, d = q.shape
     hkv = k.shape[1]
-    if hq % head_groups or hkv % head_groups:
-        raise ValueError(f"head_groups={head_groups} must divide Hq={hq} and Hkv={hkv}")
+    r = hq // hkv
+    if isinstance(head_groups, int):
+        if head_groups < 1 or hq % head_groups or hkv % head_groups:
+            raise ValueError(f"head_groups={head_groups} must divide Hq={hq} and Hkv={hkv}")
+        sizes = [hq // head_groups] * head_groups
+    else:
+        sizes = [int(x) for x in head_groups]
+        if sum(sizes) != hq or any(x <= 0 or x % r for x in sizes):
+            raise ValueError(f"head group sizes {sizes} must be multiples of Hq/Hkv={r} "
+                             f"summing to Hq={hq}")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-    gq, gk = hq // head_groups, hkv // head_groups
+    st = _streamer(dev)
     compute = torch.cuda.current_stream(dev)
-    h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-
-    def slot():
-        mk = lambda h: torch.empty(c, h, d, device=dev, dtype=torch.bfloat16)
-        return {"q": mk(gq), "k": mk(gk), "v": mk(gk), "do": mk(gq)}
-
-    slots = [slot(), slot()]
-    freed = [None, None]  # event: the slot's inputs are no longer read by compute
-    results = []
-    for g in range(head_groups):
-        s = slots[g % 2]
-        hs_q = slice(g * gq, (g + 1) * gq)
-        hs_k = slice(g * gk, (g + 1) * gk)
-        if freed[g % 2] is not None:
-            h2d.wait_event(freed[g % 2])
+    h2d, d2h = st.h2d, st.d2h
+    q0 = 0
+    for g, gq in enumerate(sizes):
+        b = g % 2
+        gk = gq // r
+        hs_q = slice(q0, q0 + gq)
+        hs_k = slice(q0 // r, q0 // r + gk)
+        q0 += gq
+        # slot b's inputs were last read by the compute of group g-2 (or the previous call)
+        if st.freed[b] is not None:
+            h2d.wait_event(st.freed[b])
+        sl = st.slots[b]
+        s = {"q": sl.get("q", (c, gq, d), torch.bfloat16, dev),
+             "k": sl.get("k", (c, gk, d), torch.bfloat16, dev),
+             "v": sl.get("v", (c, gk, d), torch.bfloat16, dev),
+             "do": sl.get("do", (c, gq, d), torch.bfloat16, dev)}
         _copy2d(s["q"], q, hs_q, True, h2d)
         _copy2d(s["k"], k, hs_k, True, h2d)
         _copy2d(s["v"], v, hs_k, True, h2d)
@@ -83,13 +115,18 @@ def attention_fwd_bwd_host(q, k, v, dout, out, lse, dq, dk, dv, *, group=None,
         loaded = torch.cuda.Event()
         loaded.record(h2d)
         compute.wait_event(loaded)
+        # workspace b's results were last read by the D2H copies of group g-2
+        if st.copied[b] is not None:
+            compute.wait_event(st.copied[b])
+        ws = st.work[b]
         o_g, lse_g = ring.ring_forward(s["q"], s["k"], s["v"], group=group, layout=layout,
-                                       softmax_scale=scale)
+                                       softmax_scale=scale, workspace=ws)
         dq_g, dk_g, dv_g = ring.ring_backward(s["do"], s["q"], s["k"], s["v"], o_g, lse_g,
-                                              group=group, layout=layout, softmax_scale=scale)
+                                              group=group, layout=layout, softmax_scale=scale,
+                                              workspace=ws)
         done = torch.cuda.Event()
         done.record(compute)
-        freed[g % 2] = done
+        st.freed[b] = done
         d2h.wait_event(done)
         _copy2d(out, o_g, hs_q, False, d2h)
         _copy2d(dq, dq_g, hs_q, False, d2h)
@@ -97,13 +134,34 @@ def attention_fwd_bwd_host(q, k, v, dout, out, lse, dq, dk, dv, *, group=None,
         _copy2d(dv, dv_g, hs_k, False, d2h)
         with torch.cuda.stream(d2h):
             lse[hs_q].copy_(lse_g, non_blocking=True)  # [gq, c] rows are contiguous
-        # keep the group's device results alive until their copies are issued/finished
-        for t in (o_g, lse_g, dq_g, dk_g, dv_g):
-            t.record_stream(d2h)
-        results.append((o_g, lse_g, dq_g, dk_g, dv_g))
+        copied = torch.cuda.Event()
+        copied.record(d2h)
+        st.copied[b] = copied
     finished = torch.cuda.Event()
     finished.record(d2h)
-    for sl in slots:
-        for t in sl.values():
-            t.record_stream(h2d)
     return finished
+
+
+class _Streamer:
+    """Per-device state the streaming API keeps across calls: the two copy streams, two
+    input slots and two ring workspaces (allocated once, grown on demand: no per-call
+    device allocation, hence no allocator synchronisation), and the events ordering
+    their reuse across groups and across calls."""
+
+    def __init__(self, dev):
+        self.h2d = torch.cuda.Stream(dev)
+        self.d2h = torch.cuda.Stream(dev)
+        self.slots = [ring.Workspace(), ring.Workspace()]
+        self.work = [ring.Workspace(), ring.Workspace()]
+        self.freed = [None, None]   # compute finished reading slot b
+        self.copied = [None, None]  # D2H finished reading workspace b
+
+
+_STREAMERS: dict = {}
+
+
+def _streamer(dev) -> _Streamer:
+    key = torch.device(dev).index if torch.device(dev).index is not None else torch.cuda.current_device()
+    if key not in _STREAMERS:
+        _STREAMERS[key] = _Streamer(dev)
+    return _STREAMERS[key]

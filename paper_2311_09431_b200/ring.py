@@ -111,6 +111,37 @@ class _Streams:
             self.compute.wait_stream(self.comm)
 
 
+class Workspace:
+    """Reusable device buffers for ring_forward / ring_backward: with a workspace the
+    calls allocate nothing (outputs are views into it, valid until the next call that
+    uses the same workspace)."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, name, shape, dtype, device, zero=False):
+        n = 1
+        for x in shape:
+            n *= int(x)
+        t = self._bufs.get(name)
+        if t is None or t.numel() < n or t.dtype != dtype or t.device != torch.device(device):
+            if t is not None and t.is_cuda:
+                # growing: the old buffer may still be in use on any stream
+                torch.cuda.synchronize(t.device)
+            t = torch.empty(max(n, 1), dtype=dtype, device=device)
+            self._bufs[name] = t
+        v = t[:n].view(*shape)
+        if zero:
+            v.zero_()
+        return v
+
+
+def _alloc(ws, name, shape, dtype, device, zero=False):
+    if ws is not None:
+        return ws.get(name, shape, dtype, device, zero)
+    return (torch.zeros if zero else torch.empty)(*shape, dtype=dtype, device=device)
+
+
 class _StepTimer:
     """CUDA-event time of each round's block kernel on the compute stream (telemetry)."""
 
@@ -141,7 +172,7 @@ class _StepTimer:
 
 def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale: float,
                  block_ops: BlockOps | None = None, stats: RingStats | None = None,
-                 count_tiles: bool = False):
+                 count_tiles: bool = False, workspace: Workspace | None = None):
     """Forward for this rank's stripe.  q [c,Hq,D], k/v [c,Hkv,D] (bf16 on GPU).
 
     Returns (out [c,Hq,D] bf16, lse [Hq,c] fp32) in local (permuted) order, like
@@ -150,9 +181,10 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     c, hq, d = q.shape
-    out = torch.empty_like(q)
-    lse = torch.empty(hq, c, device=q.device, dtype=torch.float32)
-    o_acc = None if world == 1 else torch.empty(c, hq, d, device=q.device, dtype=torch.float32)
+    ws = workspace
+    out = _alloc(ws, "out", (c, hq, d), q.dtype, q.device)
+    lse = _alloc(ws, "lse", (hq, c), torch.float32, q.device)
+    o_acc = None if world == 1 else _alloc(ws, "o_acc", (c, hq, d), torch.float32, q.device)
     tiles = torch.zeros(1, device=q.device, dtype=torch.int64) if count_tiles else None
     timer = _StepTimer(q, stats is not None)
     if world == 1:
@@ -167,7 +199,8 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
         return out, lse
     comm = _Comm(group)
     st = _Streams(q)
-    bufs = [(torch.empty_like(k), torch.empty_like(v)) for _ in range(2)]
+    bufs = [(_alloc(ws, f"kbuf{b}", k.shape, k.dtype, k.device),
+             _alloc(ws, f"vbuf{b}", v.shape, v.dtype, v.device)) for b in range(2)]
     cur = (k, v)
     for i in range(world):
         held = (rank - i) % world
@@ -199,7 +232,7 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
 
 def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped",
                   softmax_scale: float, block_ops: BlockOps | None = None,
-                  stats: RingStats | None = None):
+                  stats: RingStats | None = None, workspace: Workspace | None = None):
     """Backward for this rank's stripe -> (dq, dk, dv) bf16 in local order.
 
     K/V hop one rank per round (prefetched on the side stream); the fp32 dK/dV
@@ -211,11 +244,12 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
     c, hq, d = q.shape
     hkv = k.shape[1]
     dev = q.device
-    dsum = torch.empty(hq, c, device=dev, dtype=torch.float32)
-    dq_acc = torch.empty(c, hq, d, device=dev, dtype=torch.float32)
+    ws = workspace
+    dsum = _alloc(ws, "dsum", (hq, c), torch.float32, dev)
+    dq_acc = _alloc(ws, "dq_acc", (c, hq, d), torch.float32, dev)
     bops.bwd_preprocess(out, dout, dsum, dq_acc)
-    dk_acc = torch.zeros(c, hkv, d, device=dev, dtype=torch.float32)
-    dv_acc = torch.zeros(c, hkv, d, device=dev, dtype=torch.float32)
+    dk_acc = _alloc(ws, "dk_acc", (c, hkv, d), torch.float32, dev, zero=True)
+    dv_acc = _alloc(ws, "dv_acc", (c, hkv, d), torch.float32, dev, zero=True)
     timer = _StepTimer(q, stats is not None)
     if world == 1:
         kind = masks.block_mask(layout, 0, 0, 1)
@@ -227,8 +261,10 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
     else:
         comm = _Comm(group)
         st = _Streams(q)
-        kv_bufs = [(torch.empty_like(k), torch.empty_like(v)) for _ in range(2)]
-        dkv_bufs = [(torch.empty_like(dk_acc), torch.empty_like(dv_acc)) for _ in range(1)]
+        kv_bufs = [(_alloc(ws, f"bkbuf{b}", k.shape, k.dtype, dev),
+                    _alloc(ws, f"bvbuf{b}", v.shape, v.dtype, dev)) for b in range(2)]
+        dkv_bufs = [(_alloc(ws, "dk_spare", dk_acc.shape, torch.float32, dev),
+                     _alloc(ws, "dv_spare", dv_acc.shape, torch.float32, dev))]
         cur = (k, v)
         dcur = (dk_acc, dv_acc)
         dspare = dkv_bufs[0]
@@ -263,9 +299,9 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
         dk_acc, dv_acc = dcur
     if stats is not None:
         timer.fill(stats.rounds)
-    dq = torch.empty_like(q)
-    dk = torch.empty_like(k)
-    dv = torch.empty_like(v)
+    dq = _alloc(ws, "dq", q.shape, q.dtype, dev)
+    dk = _alloc(ws, "dk", k.shape, k.dtype, dev)
+    dv = _alloc(ws, "dv", v.shape, v.dtype, dev)
     bops.cast(dq_acc, dq)
     bops.cast(dk_acc, dk)
     bops.cast(dv_acc, dv)

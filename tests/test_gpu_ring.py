@@ -221,14 +221,16 @@ def test_ringsim_shaped_shim_matches_reference(name):
     assert got == g["stats"].tolist()
 
 
-@pytest.mark.parametrize("groups", [1, 2, 4])
+@pytest.mark.parametrize("groups", [1, 2, 4, "ramp", (2, 6)])
 def test_host_streaming_api_matches_device_api(pkg, groups):
     """host.attention_fwd_bwd_host (pinned host in/out, head groups streamed with copy /
     compute overlap) returns what the device API returns."""
     p, _ = pkg
     from paper_2311_09431_b200 import host
     c, hq, hkv, d = 1000, 8, 4, 128
-    gen = torch.Generator().manual_seed(groups)
+    gen = torch.Generator().manual_seed(7)
+    if groups == "ramp":
+        groups = host.ramp_groups(hq, hkv)
     mk = lambda h: torch.randn(c, h, d, generator=gen).bfloat16().pin_memory()
     q, k, v, do = mk(hq), mk(hkv), mk(hkv), mk(hq)
     out, dq = (torch.empty(c, hq, d, dtype=torch.bfloat16).pin_memory() for _ in range(2))
