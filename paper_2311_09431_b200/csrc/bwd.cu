@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
 #pragma unroll
           for (int kk = 0; kk < 8; kk++)
             mma_ss2(t_dk, c + kmaj(kk), hi, e + kk * 128, hi, id_kv, (it > 0 || kk > 0) ? 1u : 0u);
+          // one commit: Q stage s and the dS tile are both free once dK(it) retired
           mma_commit(&bar[B_Q_EMPTY + s]);
-          mma_commit(&bar[B_DS_EMPTY]);
         }
         __syncwarp();
         SA_TR(7);
@@ -295,6 +295,17 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       if (tr) SA_TR(8);
       tc_fence_after();
       mbar_wait(&bar[B_LSE_FULL + s], (it >> 1) & 1);
+      if (p.debug & 4) {  // perf experiments only: no compute, just the hand-offs
+        tc_fence_before();
+        mbar_arrive(&bar[B_P_READY]);
+        mbar_wait(&bar[B_DP_FULL], it & 1);
+        tc_fence_after();
+        if (it > 0) mbar_wait(&bar[B_Q_EMPTY + ((it - 1) & 1)], ((it - 1) >> 1) & 1);
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bar[B_DS_READY]);
+        continue;
+      }
       float pv[64];
 #pragma unroll
       for (int ch = 0; ch < 2; ch++) {
@@ -327,7 +338,8 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       mbar_wait(&bar[B_DP_FULL], it & 1);
       if (tr) SA_TR(11);
       tc_fence_after();
-      if (it > 0) mbar_wait(&bar[B_DS_EMPTY], (it - 1) & 1);  // dQ/dK(it-1) read dS^T
+      // dQ/dK(it-1) read dS^T: the commit after dK(it-1) (Q stage (it-1)&1's barrier)
+      if (it > 0) mbar_wait(&bar[B_Q_EMPTY + ((it - 1) & 1)], ((it - 1) >> 1) & 1);
       if (tr) SA_TR(12);
 #pragma unroll
       for (int ch = 0; ch < 2; ch++) {

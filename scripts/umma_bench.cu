@@ -12,7 +12,7 @@ __device__ int g_reps = 64;
 
 // variant: bit0 = A from TMEM, bit1 = B MN-major, N in template
 template <bool kPair, bool kTS, bool kBmn, int N>
-__global__ void bench_kernel(long long* out, int mode) {
+__global__ void bench_kernel(long long* out, int mode, const uint8_t* gsrc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
@@ -51,14 +51,15 @@ __global__ void bench_kernel(long long* out, int mode) {
   const uint32_t sa_ = smem_u32(smem), sb = smem_u32(smem + 32768);
   constexpr uint32_t kM = kPair ? 256 : 128;
   constexpr uint32_t kNc = kPair ? N / 2 : N;  // B extent held per CTA
-  const uint32_t id = idesc_bf16(kM, N, 0, kBmn ? 1 : 0);
+  const uint32_t id = idesc_bf16(kM, N, (mode & 16) ? 1 : 0, kBmn ? 1 : 0);
   constexpr uint32_t hi = sdesc_hi(1024);
   if (threadIdx.x == 0 && rank == 0) {
     long long t0 = clock64();
     const int kReps = g_reps;
     for (int r = 0; r < kReps; r++) {
       for (int kk = 0; kk < 8; kk++) {
-        const uint32_t a = sdesc_lo(sa_ + (kk >> 2) * 16384 + (kk & 3) * 32, 16);
+        const uint32_t a = (mode & 16) ? sdesc_lo(sa_ + kk * 2048, 16384)
+                                       : sdesc_lo(sa_ + (kk >> 2) * 16384 + (kk & 3) * 32, 16);
         uint32_t b;
         if (kBmn) b = sdesc_lo(sb + kk * 2048, 128 * 128);  // K rows x 64-col panels
         else b = sdesc_lo(sb + (kk >> 2) * (kNc * 128) + (kk & 3) * 32, 16);
@@ -80,6 +81,23 @@ __global__ void bench_kernel(long long* out, int mode) {
   } else if (kPair && threadIdx.x == 0) {
     mbar_wait(&bar, 0);
     done = 1;
+  } else if ((mode & 32) && warp == 1 && (threadIdx.x & 31) == 0) {
+    // background TMA-style bulk copies global -> smem (16 KB chunks, 3 in flight)
+    __shared__ uint64_t cbar[3];
+    for (int i = 0; i < 3; i++) mbar_init(&cbar[i], 1);
+    fence_barrier_init();
+    uint32_t it = 0;
+    while (!done) {
+      const int b = it % 3;
+      if (it >= 3) mbar_wait(&cbar[b], ((it / 3) - 1) & 1);
+      mbar_arrive_expect_tx(&cbar[b], 16384);
+      const uint8_t* src = gsrc + (size_t)((blockIdx.x * 7919u + it) % 4096u) * 16384;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(smem + 112 * 1024 + b * 16384)), "l"(src), "r"(16384),
+                     "r"(smem_u32(&cbar[b])) : "memory");
+      it++;
+    }
+    for (uint32_t k = it >= 3 ? it - 3 : 0; k < it; k++) mbar_wait(&cbar[k % 3], (k / 3) & 1);
   } else if ((mode & 4) && warp >= 4) {
     // softmax-like TMEM traffic: 128 columns loaded, 64 stored, per pass
     uint32_t r[128];
@@ -139,9 +157,11 @@ void run(const char* name, int grid, int mode) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  cudaLaunchKernelEx(&cfg, k, d, mode);
+  static uint8_t* gsrc = nullptr;
+  if (!gsrc) cudaMalloc(&gsrc, (size_t)4096 * 16384);
+  cudaLaunchKernelEx(&cfg, k, d, mode, (const uint8_t*)gsrc);
   cudaEventRecord(e0);
-  cudaLaunchKernelEx(&cfg, k, d, mode);
+  cudaLaunchKernelEx(&cfg, k, d, mode, (const uint8_t*)gsrc);
   cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   float ms = 0.f;
@@ -247,15 +267,14 @@ void run_seq(int shift, int reps, int commits, int mode) {
 
 int main(int argc, char** argv) {
   int reps = argc > 1 ? atoi(argv[1]) : 64;
-  for (int md : {0, 8, 1}) run_seq(0, reps, 1, md);
   cudaMemcpyToSymbol(g_reps, &reps, sizeof(int));
-  for (int mode : {1, 5, 13}) {
+  // mode bits: 1 random operands, 4 softmax-like TMEM traffic (8 warps), 16 A MN-major,
+  // 32 background bulk copies global -> smem
+  for (int mode : {1, 17, 33, 49, 37}) {
     const int grid = 148;
     run<false, false, false, 128>("1cta SS  M128 N128 Bk", grid, mode);
-    run<false, true, true, 128>("1cta TS  M128 N128 Bmn", grid, mode);
+    run<false, false, true, 128>("1cta SS  M128 N128 Bmn", grid, mode);
     run<true, false, false, 128>("pair SS M256 N128 Bk", grid, mode);
-    run<true, true, true, 128>("pair TS M256 N128 Bmn", grid, mode);
-    run<true, false, false, 256>("pair SS M256 N256 Bk", grid, mode);
   }
   return 0;
 }
