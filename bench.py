@@ -298,6 +298,20 @@ def main():
         pass
     peak_burst = peaks.get("bf16_tflops", 1590.0)
     peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
+
+    # training-step speedup (TMS) predicted from these measured attention
+    # critical paths (one layer, all heads) + the layer's non-attention FLOPs at the
+    # measured sustained GEMM rate, next to the reference's analytic model
+    if ring_cmp is not None:
+        from paper_2311_09431_b200 import costmodel as CM
+        preset = next((m for m in CM.PRESETS.values() if m.n_head == hq and m.head_dim == d),
+                      None)
+        if preset is not None:
+            mt = CM.measured_tms(preset, c, ring_cmp["ring_ms_per_step"], ms_max, peak_sus)
+            ring_cmp["tms"] = {"model": preset.name, "n_seq": n_seq, "sp": world,
+                               "measured": mt.tms, "other_ms_per_layer": mt.other_ms,
+                               "analytic_flop_weight_1": CM.tms(preset, n_seq, world, 1.0),
+                               "analytic_flop_weight_2": CM.tms(preset, n_seq, world, 2.0)}
     bwd_ms = statistics.mean(per["bwd_block"])
     fwd_ms = statistics.mean(per["fwd_block"])
     # per launch one rank processes one block of c x c pairs of one ring round; average
