@@ -40,6 +40,9 @@ namespace {
 
 constexpr uint32_t kPanelBytes = 128 * 128;  // 128 rows x 128 B
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef SA_BWD_POLY
+#define SA_BWD_POLY 0  // quads of every 8 whose exp2 runs on the FMA-pipe polynomial
+#endif
 
 struct BwdParams {
   CUtensorMap tq, tk, tv, tdo;   // bf16 [c, H, D], box 64 x 1 x 128
@@ -315,10 +318,19 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
           const float4 l4 = lds128f(lse_a + (ch * 32 + e) * 4);
-          pv[ch * 32 + e + 0] = ex2(fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x));
-          pv[ch * 32 + e + 1] = ex2(fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y));
-          pv[ch * 32 + e + 2] = ex2(fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z));
-          pv[ch * 32 + e + 3] = ex2(fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w));
+          const float x0 = fmaf(__uint_as_float(sr[e + 0]), p.scale_log2, -l4.x);
+          const float x1 = fmaf(__uint_as_float(sr[e + 1]), p.scale_log2, -l4.y);
+          const float x2 = fmaf(__uint_as_float(sr[e + 2]), p.scale_log2, -l4.z);
+          const float x3 = fmaf(__uint_as_float(sr[e + 3]), p.scale_log2, -l4.w);
+          if (((ch * 32 + e) / 4) % 8 < SA_BWD_POLY) {  // FMA-pipe exp2 for a share of quads
+            ex2_poly2(pv[ch * 32 + e + 0], pv[ch * 32 + e + 1], x0, x1);
+            ex2_poly2(pv[ch * 32 + e + 2], pv[ch * 32 + e + 3], x2, x3);
+          } else {
+            pv[ch * 32 + e + 0] = ex2(x0);
+            pv[ch * 32 + e + 1] = ex2(x1);
+            pv[ch * 32 + e + 2] = ex2(x2);
+            pv[ch * 32 + e + 3] = ex2(x3);
+          }
         }
         if (masked) {
 #pragma unroll
@@ -427,7 +439,8 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
-          tma_reduce_add_3d(&p.tdq, smem + L::kStg + (ch & 1) * kPanelBytes, 32 * ch, h, 128 * i);
+          if (!(p.debug & 8))  // perf experiments only: bit 3 stages dQ but skips the reduce
+            tma_reduce_add_3d(&p.tdq, smem + L::kStg + (ch & 1) * kPanelBytes, 32 * ch, h, 128 * i);
           bulk_commit();
         }
       }
