@@ -484,11 +484,8 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
 template <int D>
 int launch_bwd_d(BwdParams& prm, cudaStream_t st) {
   const int smem = BwdSmem<D>::kAlloc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = true;
-  }
+  static unsigned long long attr_devices = 0;
+  if (int r = set_smem_attr_once(bwd_kernel<D>, smem, &attr_devices)) return r;
   bwd_kernel<D><<<prm.n_t * prm.hkv, 512, smem, st>>>(prm);
   return check_launch("bwd_kernel");
 }

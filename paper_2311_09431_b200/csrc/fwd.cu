@@ -396,11 +396,8 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
 template <int D>
 int launch_fwd_d(FwdParams& prm, cudaStream_t st) {
   const int smem = FwdSmem<D>::kBytes;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr_set = true;
-  }
+  static unsigned long long attr_devices = 0;
+  if (int r = set_smem_attr_once(fwd_kernel<D>, smem, &attr_devices)) return r;
   const int grid = prm.n_qblk * prm.hq;
   fwd_kernel<D><<<grid, 384, smem, st>>>(prm);
   return check_launch("fwd_kernel");

@@ -437,11 +437,8 @@ int launch_fwd_pair(const void* q, const void* k, const void* v, float* o_acc, f
     cudaMemsetAsync(trace_buf, 0, 32 * 32 * sizeof(long long), st);
     prm.trace = trace_buf;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(fwd_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr_set = true;
-  }
+  static unsigned long long attr_devices = 0;
+  if (int r = set_smem_attr_once(fwd_pair_kernel, kSmemBytes, &attr_devices)) return r;
   fwd_pair_kernel<<<2 * prm.n_pair * hq, 384, kSmemBytes, st>>>(prm);
   if (tr) {
     long long hbuf[32 * 32];

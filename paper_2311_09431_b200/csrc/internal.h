@@ -8,6 +8,24 @@
 namespace sa {
 
 void set_error(const std::string& msg);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: set it once per device
+// the kernel is launched on (bit d of *mask), thread-safely.  Returns 0 or -(cudaError).
+template <typename Kernel>
+int set_smem_attr_once(Kernel kernel, int bytes, unsigned long long* mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (__atomic_load_n(mask, __ATOMIC_ACQUIRE) & bit) return 0;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    return -static_cast<int>(e);
+  }
+  __atomic_fetch_or(mask, bit, __ATOMIC_RELEASE);
+  return 0;
+}
 int fail_arg(const std::string& msg);             // returns 1
 int check_launch(const char* what);               // 0 or -(cudaError)
 void count_launch(int n = 1);

@@ -89,7 +89,15 @@ def attention_fwd_bwd_host(q, k, v, dout, out, lse, dq, dk, dv, *, group=None,
             raise ValueError(f"head group sizes {sizes} must be multiples of Hq/Hkv={r} "
                              f"summing to Hq={hq}")
     scale = 1.0 / math.sqrt(d) if softmax_scale is None else float(softmax_scale)
-    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else \
+        torch.device(device)
+    with torch.cuda.device(dev):  # copies and kernels go to the current device
+        return _stream_groups(q, k, v, dout, out, lse, dq, dk, dv, sizes, r, c, d, scale, dev,
+                              group, layout)
+
+
+def _stream_groups(q, k, v, dout, out, lse, dq, dk, dv, sizes, r, c, d, scale, dev, group,
+                   layout):
     st = _streamer(dev)
     compute = torch.cuda.current_stream(dev)
     h2d, d2h = st.h2d, st.d2h

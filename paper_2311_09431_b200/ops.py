@@ -33,6 +33,11 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
+def _on(t: torch.Tensor):
+    """The CUDA runtime launches on the CURRENT device: make it the tensor's."""
+    return torch.cuda.device(t.device)
+
+
 def permute(src: torch.Tensor, dst: torch.Tensor, n_dev: int, scheme: int, direction: int,
             device: int = -1) -> torch.Tensor:
     """K1: Layout.partition / Layout.gather (layout.py:81-117) of whole rows, bit-exact."""
@@ -43,8 +48,9 @@ def permute(src: torch.Tensor, dst: torch.Tensor, n_dev: int, scheme: int, direc
     else:
         n_seq = dst.shape[0]
     row_bytes = src[0].numel() * src.element_size() if src.dim() > 1 else src.element_size()
-    _lib.check(_lib.lib().sa_permute(src.data_ptr(), dst.data_ptr(), n_seq, n_dev, row_bytes,
-                                     scheme, direction, device, _stream(src)), "sa_permute")
+    with _on(src):
+        _lib.check(_lib.lib().sa_permute(src.data_ptr(), dst.data_ptr(), n_seq, n_dev, row_bytes,
+                                         scheme, direction, device, _stream(src)), "sa_permute")
     return dst
 
 
@@ -62,10 +68,11 @@ def fwd_block(q, k, v, o_acc, lse, out, softmax_scale: float, mask_kind: int, fi
     hkv = k.shape[1]
     if k.shape != (c, hkv, d) or v.shape != (c, hkv, d):
         raise ValueError(f"k/v must be [{c}, hkv, {d}], got {tuple(k.shape)} / {tuple(v.shape)}")
-    _lib.check(_lib.lib().sa_fwd_block(
-        q.data_ptr(), k.data_ptr(), v.data_ptr(), _ptr(o_acc), lse.data_ptr(), _ptr(out), c, hq,
-        hkv, d, float(softmax_scale), int(mask_kind), int(first_step), int(last_step),
-        _ptr(tiles_computed), _stream(q)), "sa_fwd_block")
+    with _on(q):
+        _lib.check(_lib.lib().sa_fwd_block(
+            q.data_ptr(), k.data_ptr(), v.data_ptr(), _ptr(o_acc), lse.data_ptr(), _ptr(out), c, hq,
+            hkv, d, float(softmax_scale), int(mask_kind), int(first_step), int(last_step),
+            _ptr(tiles_computed), _stream(q)), "sa_fwd_block")
 
 
 def bwd_preprocess(out, dout, dsum, dq_acc):
@@ -74,9 +81,10 @@ def bwd_preprocess(out, dout, dsum, dq_acc):
     _need_cuda("dsum", dsum, torch.float32)
     _need_cuda("dq_acc", dq_acc, torch.float32)
     c, hq, d = out.shape
-    _lib.check(_lib.lib().sa_bwd_preprocess(out.data_ptr(), dout.data_ptr(), dsum.data_ptr(),
-                                            dq_acc.data_ptr(), c, hq, d, _stream(out)),
-               "sa_bwd_preprocess")
+    with _on(out):
+        _lib.check(_lib.lib().sa_bwd_preprocess(out.data_ptr(), dout.data_ptr(), dsum.data_ptr(),
+                                                dq_acc.data_ptr(), c, hq, d, _stream(out)),
+                   "sa_bwd_preprocess")
 
 
 def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: float,
@@ -88,10 +96,11 @@ def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: f
         _need_cuda(n, t, torch.float32)
     c, hq, d = q.shape
     hkv = k.shape[1]
-    _lib.check(_lib.lib().sa_bwd_block(
-        q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(), dsum.data_ptr(),
-        dq_acc.data_ptr(), dk_acc.data_ptr(), dv_acc.data_ptr(), c, hq, hkv, d,
-        float(softmax_scale), int(mask_kind), _stream(q)), "sa_bwd_block")
+    with _on(q):
+        _lib.check(_lib.lib().sa_bwd_block(
+            q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(), dsum.data_ptr(),
+            dq_acc.data_ptr(), dk_acc.data_ptr(), dv_acc.data_ptr(), c, hq, hkv, d,
+            float(softmax_scale), int(mask_kind), _stream(q)), "sa_bwd_block")
 
 
 def cast_f32_bf16(src: torch.Tensor, dst: torch.Tensor) -> torch.Tensor:
@@ -99,8 +108,9 @@ def cast_f32_bf16(src: torch.Tensor, dst: torch.Tensor) -> torch.Tensor:
     _need_cuda("dst", dst, torch.bfloat16)
     if src.numel() != dst.numel():
         raise ValueError("cast size mismatch")
-    _lib.check(_lib.lib().sa_cast_f32_bf16(src.data_ptr(), dst.data_ptr(), src.numel(),
-                                           _stream(src)), "sa_cast_f32_bf16")
+    with _on(src):
+        _lib.check(_lib.lib().sa_cast_f32_bf16(src.data_ptr(), dst.data_ptr(), src.numel(),
+                                               _stream(src)), "sa_cast_f32_bf16")
     return dst
 
 
@@ -111,8 +121,9 @@ def probe_umma(a, b, v):
         if t.shape != (128, 128):
             raise ValueError("probe tiles are 128x128")
     s, o, y = (torch.empty(128, 128, device=a.device, dtype=torch.float32) for _ in range(3))
-    _lib.check(_lib.lib().sa_probe_umma(a.data_ptr(), b.data_ptr(), v.data_ptr(), s.data_ptr(),
-                                        o.data_ptr(), y.data_ptr(), _stream(a)), "sa_probe_umma")
+    with _on(a):
+        _lib.check(_lib.lib().sa_probe_umma(a.data_ptr(), b.data_ptr(), v.data_ptr(), s.data_ptr(),
+                                            o.data_ptr(), y.data_ptr(), _stream(a)), "sa_probe_umma")
     return s, o, y
 
 
@@ -122,6 +133,7 @@ def probe_pair(a, b, v):
     for n, t in (("a", a), ("b", b), ("v", v)):
         _need_cuda(n, t, torch.bfloat16)
     s, o, s2 = (torch.empty(256, 128, device=a.device, dtype=torch.float32) for _ in range(3))
-    _lib.check(_lib.lib().sa_probe_pair(a.data_ptr(), b.data_ptr(), v.data_ptr(), s.data_ptr(),
-                                        o.data_ptr(), s2.data_ptr(), _stream(a)), "sa_probe_pair")
+    with _on(a):
+        _lib.check(_lib.lib().sa_probe_pair(a.data_ptr(), b.data_ptr(), v.data_ptr(), s.data_ptr(),
+                                            o.data_ptr(), s2.data_ptr(), _stream(a)), "sa_probe_pair")
     return s, o, s2
