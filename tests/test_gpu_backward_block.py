@@ -83,3 +83,54 @@ def test_backward_accumulates_into_travelling_buffers(ops):
     torch.cuda.synchronize()
     for a, b in zip(once, bufs):
         assert torch.allclose(2 * a, b, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("d", [128, 64])
+def test_backward_growing_scores(ops, d):
+    """Scores that grow along the keys (s(x, y) = 0.5 y, the forward's rescale stress case):
+    P recomputed from the global LSE stays finite and the gradients match."""
+    c, h, kind = 1024, 2, 2
+    gen = torch.Generator(device="cuda").manual_seed(5 + d)
+    q = torch.ones(c, h, d, device="cuda").bfloat16()
+    ramp = (0.5 * torch.arange(c, device="cuda", dtype=torch.float32) / d)[:, None, None]
+    k = (ramp * torch.ones(c, h, d, device="cuda")).bfloat16()
+    v = torch.randn(c, h, d, device="cuda", generator=gen).bfloat16()
+    do = torch.randn(c, h, d, device="cuda", generator=gen).bfloat16()
+    qn, kn, vn, don = (t.float().cpu().numpy().astype(np.float64) for t in (q, k, v, do))
+    o_ref, lse_ref = oracle_fwd_block(qn, kn, vn, kind, 1.0)
+    out = torch.tensor(o_ref, device="cuda").bfloat16()
+    outn = out.float().cpu().numpy().astype(np.float64)
+    lse = torch.tensor(lse_ref, device="cuda", dtype=torch.float32).contiguous()
+    dsum = torch.empty(h, c, device="cuda")
+    dq = torch.empty(c, h, d, device="cuda")
+    dk = torch.zeros(c, h, d, device="cuda")
+    dv = torch.zeros(c, h, d, device="cuda")
+    ops.bwd_preprocess(out, do, dsum, dq)
+    ops.bwd_block(q, k, v, do, lse, dsum, dq, dk, dv, 1.0, kind)
+    torch.cuda.synchronize()
+    dsum_ref = np.einsum("shd,shd->hs", don, outn)
+    want = R.block_backward(qn, kn, vn, don, lse_ref.astype(np.float32).astype(np.float64),
+                            dsum_ref, kind, 1.0)
+    # dQ = sum_y dS(x, y) K_y with sum_y dS = 0 and K growing with y is ill-conditioned
+    # (cancellation), so for dQ the reference arithmetic rounds dS to bf16 exactly as the
+    # kernel's MMA operand does; dK / dV are compared with the plain fp64 restatement.
+    s_ = np.einsum("xhd,yhd->hxy", qn, kn)
+    x_i, y_i = np.meshgrid(np.arange(c), np.arange(c), indexing="ij")
+    p_ = np.where((y_i <= x_i)[None], np.exp(s_ - lse_ref.astype(np.float32)[:, :, None]), 0.0)
+    dp_ = np.einsum("xhd,yhd->hxy", don, vn)
+    ds_ = R.bf16_round(p_ * (dp_ - dsum_ref[:, :, None])).astype(np.float64)
+    dq_bf16ds = np.einsum("hxy,yhd->xhd", ds_, kn)
+    # per element: a few bf16 ulps of every |dS K| term (P itself differs from the fp64
+    # value by fp32 rounding, which can move a dS element across a bf16 rounding boundary)
+    cond = np.einsum("hxy,yhd->xhd", np.abs(ds_), np.abs(kn))
+    g = dq.cpu().numpy()
+    assert np.isfinite(g).all()
+    assert np.all(np.abs(g - dq_bf16ds) <= 2.0 ** -6 * cond + 1e-3), \
+        float(np.max(np.abs(g - dq_bf16ds) - 2.0 ** -6 * cond))
+    # dK / dV reach |values| ~ 20 here: the max-abs bar scales with the output magnitude
+    for name, got, w in (("dk", dk, want[1]), ("dv", dv, want[2])):
+        g = got.cpu().numpy()
+        assert np.isfinite(g).all(), name
+        bar = MAX_ABS * max(1.0, float(np.max(np.abs(w))))
+        assert np.max(np.abs(g - w)) <= bar, (name, np.max(np.abs(g - w)))
+        assert rel_l2(g, w) <= REL_L2, (name, rel_l2(g, w))

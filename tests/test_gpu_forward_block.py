@@ -132,3 +132,31 @@ def test_fully_masked_step_keeps_state(ops):
     out1, lse1, _ = run_block(ops, q, k, v, 2, 0.125)
     assert torch.equal(lse, lse0)
     assert np.array_equal(out.float().cpu().numpy(), out1)
+
+
+@pytest.mark.parametrize("d", [128, 64])
+@pytest.mark.parametrize("kind", [2, 1])
+def test_extreme_and_growing_scores(ops, d, kind):
+    """The reference's extreme-score stability test (tests/test_attention.py:289-305) at
+    kernel scale: scores spanning hundreds (deep exp underflow, no inf / NaN), and scores
+    that grow along the keys so the running max rises by far more than the lazy-rescale
+    threshold in every 128-key tile (the O rescale path runs every step)."""
+    c, h = 1024, 2
+    g = torch.Generator(device="cuda").manual_seed(11 + d + kind)
+    # (a) wide scores: |q.k| up to a few hundred
+    q = (torch.rand(c, h, d, device="cuda", generator=g) * 10 - 5).bfloat16()
+    k = (torch.rand(c, h, d, device="cuda", generator=g) * 10 - 5).bfloat16()
+    v = torch.randn(c, h, d, device="cuda", generator=g).bfloat16()
+    # (b) growing scores: s(x, y) = 0.5 y for every query
+    qg = torch.ones(c, h, d, device="cuda").bfloat16()
+    ramp = (0.5 * torch.arange(c, device="cuda", dtype=torch.float32) / d)[:, None, None]
+    kg = (ramp * torch.ones(c, h, d, device="cuda")).bfloat16()
+    for qq, kk in ((q, k), (qg, kg)):
+        out, lse, _ = run_block(ops, qq, kk, v, kind, 1.0)
+        assert np.isfinite(out).all() and np.isfinite(lse).all()
+        o_ref, lse_ref = block_ref(qq.float().cpu().numpy(), kk.float().cpu().numpy(),
+                                   v.float().cpu().numpy(), kind, 1.0)
+        assert np.max(np.abs(out - o_ref)) <= O_MAX_ABS
+        assert rel_l2(out, o_ref) <= O_REL_L2
+        # relative LSE bound: the scores themselves reach hundreds
+        assert np.max(np.abs(lse - lse_ref) / np.maximum(1.0, np.abs(lse_ref))) <= LSE_ABS
