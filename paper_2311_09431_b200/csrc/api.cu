@@ -127,6 +127,8 @@ int sa_fwd_block(const void* q, const void* k, const void* v, float* o_acc, floa
   if (int r = check_heads(c, hq, hkv, d)) return r;
   if (!q || !k || !v || !lse) return fail_arg("null q/k/v/lse");
   if (!aligned16(q) || !aligned16(k) || !aligned16(v)) return fail_arg("q/k/v must be 16B aligned");
+  if ((o_acc && !aligned16(o_acc)) || (out && !aligned16(out)))
+    return fail_arg("o_acc/out must be 16B aligned");  // vector epilogue loads / stores
   if (!(first_step && last_step) && !o_acc) return fail_arg("o_acc required across ring steps");
   if (last_step && !out) return fail_arg("out required on the last step");
   if (mask_kind < 0 || mask_kind > 3) return fail_arg("bad mask kind");
@@ -159,8 +161,9 @@ int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, 
   if (int r = check_heads(c, hq, hkv, d)) return r;
   if (!q || !k || !v || !dout || !lse || !dsum || !dq_acc || !dk_acc || !dv_acc)
     return fail_arg("null pointer");
-  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout))
-    return fail_arg("q/k/v/dout must be 16B aligned");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq_acc) ||
+      !aligned16(dk_acc) || !aligned16(dv_acc))
+    return fail_arg("q/k/v/dout and the accumulators must be 16B aligned");
   if (mask_kind < 0 || mask_kind > 3) return fail_arg("bad mask kind");
   if (!(softmax_scale > 0.f)) return fail_arg("softmax_scale must be > 0");
   if (mask_kind == SA_MASK_FULLY_MASKED) return 0;

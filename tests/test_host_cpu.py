@@ -105,6 +105,13 @@ def test_c_abi_rejects_bad_arguments_without_launching():
     assert lib.sa_fwd_block(16, 16, 16, None, 16, 16, 128, 3, 2, 128, 0.1, 2, 1, 1, None, None) > 0
     assert lib.sa_fwd_block(16, 16, 16, None, 16, 16, 128, 2, 2, 128, 0.1, 7, 1, 1, None, None) > 0
     assert lib.sa_bwd_block(16, 16, 16, 16, 16, 16, 16, 16, 16, 128, 2, 2, 128, -1.0, 2, None) > 0
+    # misaligned operands / outputs (vector epilogue, TMA) are rejected before any launch
+    assert lib.sa_fwd_block(18, 16, 16, None, 16, 16, 128, 2, 2, 128, 0.1, 2, 1, 1, None, None) > 0
+    assert lib.sa_fwd_block(16, 16, 16, 20, 16, 16, 128, 2, 2, 128, 0.1, 2, 0, 1, None, None) > 0
+    assert b"aligned" in lib.sa_last_error()
+    assert lib.sa_fwd_block(16, 16, 16, None, 16, 24, 128, 2, 2, 128, 0.1, 2, 1, 1, None, None) > 0
+    assert lib.sa_bwd_block(16, 16, 16, 16, 16, 16, 16, 20, 16, 128, 2, 2, 128, 0.1, 2, None) > 0
+    assert b"aligned" in lib.sa_last_error()
 
 
 def test_product_has_no_cpu_fallback():
