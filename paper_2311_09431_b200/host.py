@@ -116,32 +116,40 @@ def _stream_groups(q, k, v, dout, out, lse, dq, dk, dv, sizes, r, c, d, scale, d
              "k": sl.get("k", (c, gk, d), torch.bfloat16, dev),
              "v": sl.get("v", (c, gk, d), torch.bfloat16, dev),
              "do": sl.get("do", (c, gq, d), torch.bfloat16, dev)}
+        # forward inputs first: the forward starts while dO is still on the wire
         _copy2d(s["q"], q, hs_q, True, h2d)
         _copy2d(s["k"], k, hs_k, True, h2d)
         _copy2d(s["v"], v, hs_k, True, h2d)
+        fwd_in = torch.cuda.Event()
+        fwd_in.record(h2d)
         _copy2d(s["do"], dout, hs_q, True, h2d)
-        loaded = torch.cuda.Event()
-        loaded.record(h2d)
-        compute.wait_event(loaded)
+        bwd_in = torch.cuda.Event()
+        bwd_in.record(h2d)
+        compute.wait_event(fwd_in)
         # workspace b's results were last read by the D2H copies of group g-2
         if st.copied[b] is not None:
             compute.wait_event(st.copied[b])
         ws = st.work[b]
         o_g, lse_g = ring.ring_forward(s["q"], s["k"], s["v"], group=group, layout=layout,
                                        softmax_scale=scale, workspace=ws)
+        fwd_done = torch.cuda.Event()
+        fwd_done.record(compute)
+        compute.wait_event(bwd_in)
         dq_g, dk_g, dv_g = ring.ring_backward(s["do"], s["q"], s["k"], s["v"], o_g, lse_g,
                                               group=group, layout=layout, softmax_scale=scale,
                                               workspace=ws)
         done = torch.cuda.Event()
         done.record(compute)
         st.freed[b] = done
-        d2h.wait_event(done)
+        # O and LSE leave while the backward runs; the gradients once it is done
+        d2h.wait_event(fwd_done)
         _copy2d(out, o_g, hs_q, False, d2h)
+        with torch.cuda.stream(d2h):
+            lse[hs_q].copy_(lse_g, non_blocking=True)  # [gq, c] rows are contiguous
+        d2h.wait_event(done)
         _copy2d(dq, dq_g, hs_q, False, d2h)
         _copy2d(dk, dk_g, hs_k, False, d2h)
         _copy2d(dv, dv_g, hs_k, False, d2h)
-        with torch.cuda.stream(d2h):
-            lse[hs_q].copy_(lse_g, non_blocking=True)  # [gq, c] rows are contiguous
         copied = torch.cuda.Event()
         copied.record(d2h)
         st.copied[b] = copied
