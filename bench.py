@@ -210,6 +210,9 @@ def main():
         def bwd_block(self, *a):
             self._wrap("bwd_block", super().bwd_block, *a)
 
+        def bwd_block_final(self, *a):  # the N = 1 backward (bf16 dK / dV out of the kernel)
+            self._wrap("bwd_block", super().bwd_block_final, *a)
+
         def bwd_preprocess(self, *a):
             self._wrap("bwd_preprocess", super().bwd_preprocess, *a)
 

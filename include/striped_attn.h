@@ -95,6 +95,15 @@ int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, 
                  void* stream);
 
 /* dst_bf16[i] = bf16(src[i]) (finalises dq/dk/dv accumulators and skipped last steps). */
+/* Single-step backward ("final"): as sa_bwd_block, but dK / dV are written (not added)
+ * as bf16 [c, Hkv, D] straight from the kernel's accumulators: no fp32 accumulators, no
+ * zero-fill, no cast.  For a block that is the ONLY contribution to dK / dV (N = 1, or
+ * the caller's own non-ring use); the ring's travelling accumulators use sa_bwd_block. */
+int sa_bwd_block_final(const void* q, const void* k, const void* v, const void* dout,
+                       const float* lse, const float* dsum, float* dq_acc, void* dk, void* dv,
+                       int64_t c, int32_t hq, int32_t hkv, int32_t d, float softmax_scale,
+                       int32_t mask_kind, void* stream);
+
 int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
 
 /* Strided host<->device row copy (cudaMemcpy2DAsync): `height` rows of `width` bytes,

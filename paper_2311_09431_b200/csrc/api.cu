@@ -171,6 +171,29 @@ int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, 
                     softmax_scale, mask_kind, static_cast<cudaStream_t>(stream));
 }
 
+int sa_bwd_block_final(const void* q, const void* k, const void* v, const void* dout,
+                       const float* lse, const float* dsum, float* dq_acc, void* dk, void* dv,
+                       int64_t c, int32_t hq, int32_t hkv, int32_t d, float softmax_scale,
+                       int32_t mask_kind, void* stream) {
+  if (int r = check_heads(c, hq, hkv, d)) return r;
+  if (!q || !k || !v || !dout || !lse || !dsum || !dq_acc || !dk || !dv)
+    return fail_arg("null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq_acc) ||
+      !aligned16(dk) || !aligned16(dv))
+    return fail_arg("q/k/v/dout, dq_acc and dk/dv must be 16B aligned");
+  if (mask_kind < 0 || mask_kind > 3) return fail_arg("bad mask kind");
+  if (!(softmax_scale > 0.f)) return fail_arg("softmax_scale must be > 0");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (mask_kind == SA_MASK_FULLY_MASKED) {  // no pair: the gradients are zero
+    const size_t bytes = static_cast<size_t>(c) * hkv * d * 2;
+    if (cudaMemsetAsync(dk, 0, bytes, st) != cudaSuccess || cudaMemsetAsync(dv, 0, bytes, st) != cudaSuccess)
+      return check_launch("memset dk/dv");
+    return 0;
+  }
+  return launch_bwd(q, k, v, dout, lse, dsum, dq_acc, nullptr, nullptr, c, hq, hkv, d,
+                    softmax_scale, mask_kind, st, dk, dv);
+}
+
 int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream) {
   if (!src || !dst || n < 0) return fail_arg("bad cast arguments");
   if (n == 0) return 0;

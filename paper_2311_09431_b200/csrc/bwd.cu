@@ -49,6 +49,10 @@ struct BwdParams {
   CUtensorMap tdq, tdk, tdv;     // fp32 [c, H, D], box 32 x 1 x 128 (reduce-add)
   const float* lse;
   const float* dsum;
+  // "final" mode (single-step backward, sa_bwd_block_final): dK / dV are written once as
+  // bf16 straight from TMEM instead of reduce-added into fp32 accumulators
+  __nv_bfloat16* dk_out;
+  __nv_bfloat16* dv_out;
   int c, hq, hkv, n_t;
   float scale, scale_log2;
   int kind;
@@ -85,6 +89,28 @@ __device__ __forceinline__ bool allowed_bwd(int kind, int x, int y, int c) {
   if (kind == SA_MASK_CAUSAL_INCLUSIVE) return y <= x;
   if (kind == SA_MASK_CAUSAL_EXCLUSIVE) return y < x;
   return true;
+}
+
+// One key row (TMEM lane) of a dK / dV accumulator -> bf16 global row y of kv head g.
+template <int D>
+__device__ __forceinline__ void store_row_bf16(__nv_bfloat16* base, uint32_t t_row, float scale,
+                                               int y, int g, const BwdParams& p) {
+  __nv_bfloat16* dst = base + ((int64_t)y * p.hkv + g) * D;
+  const bool live = y < p.c;
+#pragma unroll 1
+  for (int ch = 0; ch < D / 32; ch++) {
+    uint32_t o[32];
+    SA_TMEM_LD32(t_row + ch * 32, o);
+    tmem_ld_wait();
+    if (!live) continue;
+    uint4* d4 = reinterpret_cast<uint4*>(dst + ch * 32);
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const float* f = reinterpret_cast<const float*>(o + 8 * i);
+      d4[i] = make_uint4(pack_bf16(f[0] * scale, f[1] * scale), pack_bf16(f[2] * scale, f[3] * scale),
+                         pack_bf16(f[4] * scale, f[5] * scale), pack_bf16(f[6] * scale, f[7] * scale));
+    }
+  }
 }
 
 template <int D>
@@ -384,6 +410,9 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       // ---------------------------------------------------------- dV epilogue
       mbar_wait(&bar[B_KV_DONE], 0);
       tc_fence_after();
+      if (p.dv_out) {
+        store_row_bf16<D>(p.dv_out, t_dv + lane_off, 1.f, 128 * j + static_cast<int>(row), g, p);
+      } else {
       const uint32_t stage = sbase + L::kQ;  // Q stages are free now
 #pragma unroll 1
       for (int ch = 0; ch < kChunks; ch++) {
@@ -402,6 +431,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
           tma_reduce_add_3d(&p.tdv, smem + L::kQ + ch * kPanelBytes, 32 * ch, g, 128 * j);
         bulk_commit();
         bulk_wait<0>();
+      }
       }
     }
   } else {
@@ -450,6 +480,9 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
     // ------------------------------------------------------------ dK epilogue
     mbar_wait(&bar[B_KV_DONE], 0);
     tc_fence_after();
+    if (p.dk_out) {
+      store_row_bf16<D>(p.dk_out, t_dk + lane_off, p.scale, 128 * j + static_cast<int>(row), g, p);
+    } else {
     const uint32_t kst = sbase + L::kDO;  // dO + dS buffers (contiguous) are free now
 #pragma unroll 1
     for (int ch = 0; ch < kChunks; ch++) {
@@ -471,6 +504,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         tma_reduce_add_3d(&p.tdk, smem + L::kDO + ch * kPanelBytes, 32 * ch, g, 128 * j);
       bulk_commit();
       bulk_wait<0>();
+    }
     }
   }
   tc_fence_before();
@@ -494,15 +528,20 @@ int launch_bwd_d(BwdParams& prm, cudaStream_t st) {
 
 int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                const float* dsum, float* dq, float* dk, float* dv, int64_t c, int32_t hq,
-               int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st) {
+               int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st,
+               void* dk_out, void* dv_out) {
   BwdParams prm;
+  prm.dk_out = static_cast<__nv_bfloat16*>(dk_out);
+  prm.dv_out = static_cast<__nv_bfloat16*>(dv_out);
   if (int r = make_tmap_rows(&prm.tq, q, c, hq, d, 128)) return r;
   if (int r = make_tmap_rows(&prm.tk, k, c, hkv, d, 128)) return r;
   if (int r = make_tmap_rows(&prm.tv, v, c, hkv, d, 128)) return r;
   if (int r = make_tmap_rows(&prm.tdo, dout, c, hq, d, 128)) return r;
   if (int r = make_tmap_rows_f32(&prm.tdq, dq, c, hq, d, 128)) return r;
-  if (int r = make_tmap_rows_f32(&prm.tdk, dk, c, hkv, d, 128)) return r;
-  if (int r = make_tmap_rows_f32(&prm.tdv, dv, c, hkv, d, 128)) return r;
+  if (!dk_out)
+    if (int r = make_tmap_rows_f32(&prm.tdk, dk, c, hkv, d, 128)) return r;
+  if (!dv_out)
+    if (int r = make_tmap_rows_f32(&prm.tdv, dv, c, hkv, d, 128)) return r;
   prm.lse = lse;
   prm.dsum = dsum;
   prm.c = static_cast<int>(c);

@@ -55,9 +55,11 @@ int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float*
                int32_t first, int32_t last, int64_t* tiles, cudaStream_t st);
 int launch_bwd_pre(const void* out, const void* dout, float* dsum, float* dq_acc, int64_t c,
                    int32_t hq, int32_t d, cudaStream_t st);
+// dk_out / dv_out non-null: "final" mode, dK / dV written as bf16 (dk / dv unused)
 int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                const float* dsum, float* dq, float* dk, float* dv, int64_t c, int32_t hq,
-               int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st);
+               int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st,
+               void* dk_out = nullptr, void* dv_out = nullptr);
 int launch_cast(const float* src, void* dst, int64_t n, cudaStream_t st);
 int launch_fill_state(float* o_acc, float* lse, int64_t c, int32_t hq, int32_t d, cudaStream_t st);
 

@@ -103,6 +103,23 @@ def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: f
             float(softmax_scale), int(mask_kind), _stream(q)), "sa_bwd_block")
 
 
+def bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, softmax_scale: float,
+                    mask_kind: int):
+    """K5 for a block that is the only contribution to dK / dV: dk / dv (bf16 [c, Hkv, D])
+    are written, not accumulated (sa_bwd_block_final)."""
+    for n, t in (("q", q), ("k", k), ("v", v), ("dout", dout), ("dk", dk), ("dv", dv)):
+        _need_cuda(n, t, torch.bfloat16)
+    for n, t in (("lse", lse), ("dsum", dsum), ("dq_acc", dq_acc)):
+        _need_cuda(n, t, torch.float32)
+    c, hq, d = q.shape
+    hkv = k.shape[1]
+    with _on(q):
+        _lib.check(_lib.lib().sa_bwd_block_final(
+            q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+            dsum.data_ptr(), dq_acc.data_ptr(), dk.data_ptr(), dv.data_ptr(), c, hq, hkv, d,
+            float(softmax_scale), int(mask_kind), _stream(q)), "sa_bwd_block_final")
+
+
 def cast_f32_bf16(src: torch.Tensor, dst: torch.Tensor) -> torch.Tensor:
     _need_cuda("src", src, torch.float32)
     _need_cuda("dst", dst, torch.bfloat16)

@@ -43,6 +43,10 @@ class BlockOps:
     def bwd_block(self, q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind):
         self._ops.bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind)
 
+    def bwd_block_final(self, q, k, v, dout, lse, dsum, dq_acc, dk, dv, scale, kind):
+        """Single-step backward: bf16 dK / dV written directly (no accumulators / casts)."""
+        self._ops.bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, scale, kind)
+
     def cast(self, src, dst):
         self._ops.cast_f32_bf16(src, dst)
 
@@ -248,9 +252,23 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
     dsum = _alloc(ws, "dsum", (hq, c), torch.float32, dev)
     dq_acc = _alloc(ws, "dq_acc", (c, hq, d), torch.float32, dev)
     bops.bwd_preprocess(out, dout, dsum, dq_acc)
+    timer = _StepTimer(q, stats is not None)
+    if world == 1 and hasattr(bops, "bwd_block_final"):
+        # one step: dK / dV come out of the kernel as bf16 (no fp32 accumulators / casts)
+        kind = masks.block_mask(layout, 0, 0, 1)
+        dk = _alloc(ws, "dk", k.shape, k.dtype, dev)
+        dv = _alloc(ws, "dv", v.shape, v.dtype, dev)
+        timer.start()
+        bops.bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, softmax_scale, kind)
+        timer.stop()
+        if stats is not None:
+            stats.rounds.append(StepRecord(0, 0, int(kind)))
+            timer.fill(stats.rounds)
+        dq = _alloc(ws, "dq", q.shape, q.dtype, dev)
+        bops.cast(dq_acc, dq)
+        return dq, dk, dv
     dk_acc = _alloc(ws, "dk_acc", (c, hkv, d), torch.float32, dev, zero=True)
     dv_acc = _alloc(ws, "dv_acc", (c, hkv, d), torch.float32, dev, zero=True)
-    timer = _StepTimer(q, stats is not None)
     if world == 1:
         kind = masks.block_mask(layout, 0, 0, 1)
         timer.start()

@@ -134,3 +134,28 @@ def test_backward_growing_scores(ops, d):
         bar = MAX_ABS * max(1.0, float(np.max(np.abs(w))))
         assert np.max(np.abs(g - w)) <= bar, (name, np.max(np.abs(g - w)))
         assert rel_l2(g, w) <= REL_L2, (name, rel_l2(g, w))
+
+
+@pytest.mark.parametrize("kind", [2, 3, 1, 0])
+@pytest.mark.parametrize("c,hq,hkv,d", [(1000, 4, 2, 128), (384, 2, 2, 64)])
+def test_final_mode_equals_accumulate_then_cast(ops, kind, c, hq, hkv, d):
+    """sa_bwd_block_final (bf16 dK / dV straight from TMEM) == sa_bwd_block into zeroed fp32
+    accumulators + cast, bit for bit; dQ identical up to the reduce-add order."""
+    gen = torch.Generator(device="cuda").manual_seed(c + kind)
+    q, do = (torch.randn(c, hq, d, device="cuda", generator=gen).bfloat16() for _ in range(2))
+    k, v = (torch.randn(c, hkv, d, device="cuda", generator=gen).bfloat16() for _ in range(2))
+    lse = (torch.randn(hq, c, device="cuda", generator=gen).abs() + 3.0).contiguous()
+    dsum = torch.randn(hq, c, device="cuda", generator=gen)
+    scale = 1.0 / math.sqrt(d)
+    dq_a = torch.zeros(c, hq, d, device="cuda")
+    dk_a = torch.zeros(c, hkv, d, device="cuda")
+    dv_a = torch.zeros(c, hkv, d, device="cuda")
+    ops.bwd_block(q, k, v, do, lse, dsum, dq_a, dk_a, dv_a, scale, kind)
+    dq_b = torch.zeros(c, hq, d, device="cuda")
+    dk_b = torch.full((c, hkv, d), 3.0, device="cuda").bfloat16()  # must be overwritten
+    dv_b = torch.full((c, hkv, d), 3.0, device="cuda").bfloat16()
+    ops.bwd_block_final(q, k, v, do, lse, dsum, dq_b, dk_b, dv_b, scale, kind)
+    torch.cuda.synchronize()
+    assert torch.equal(dk_b.view(torch.int16), dk_a.bfloat16().view(torch.int16))
+    assert torch.equal(dv_b.view(torch.int16), dv_a.bfloat16().view(torch.int16))
+    assert (dq_a - dq_b).abs().max().item() <= 1e-4 * max(1.0, dq_a.abs().max().item())
