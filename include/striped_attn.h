@@ -95,6 +95,16 @@ int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, 
                  void* stream);
 
 /* dst_bf16[i] = bf16(src[i]) (finalises dq/dk/dv accumulators and skipped last steps). */
+/* sa_bwd_block restricted to the keys [key_row_begin, key_row_end) of the held stripe
+ * (128-aligned; the end may be c): only those dK / dV rows and their dQ contributions.
+ * The ring launches a block in parts so each part's dK / dV rows can travel to the next
+ * rank while the next part computes. */
+int sa_bwd_block_range(const void* q, const void* k, const void* v, const void* dout,
+                       const float* lse, const float* dsum, float* dq_acc, float* dk_acc,
+                       float* dv_acc, int64_t c, int32_t hq, int32_t hkv, int32_t d,
+                       float softmax_scale, int32_t mask_kind, int32_t key_row_begin,
+                       int32_t key_row_end, void* stream);
+
 /* Single-step backward ("final"): as sa_bwd_block, but dK / dV are written (not added)
  * as bf16 [c, Hkv, D] straight from the kernel's accumulators: no fp32 accumulators, no
  * zero-fill, no cast.  For a block that is the ONLY contribution to dK / dV (N = 1, or

@@ -438,12 +438,14 @@ def dense_backward(q, k, v, do, softmax_scale: float, dtype=np.float64):
     return dq, dk, dv
 
 
-def block_backward(q, k, v, do, lse, dsum, kind: int, softmax_scale: float, dtype=np.float64):
+def block_backward(q, k, v, do, lse, dsum, kind: int, softmax_scale: float, dtype=np.float64,
+                   key_rows=None):
     """NOT REFERENCE.  One (rank, step) block of the ring backward: recompute
     P = exp(scale*QK^T - lse) under the block mask (same predicate as the
     forward, attention.py:172-183) with the GLOBAL lse, and return this block's
     (dq, dk, dv) contributions.  q/do/lse/dsum belong to the query stripe,
-    k/v to the held key stripe."""
+    k/v to the held key stripe.  ``key_rows=(r0, r1)`` keeps only the keys in
+    [r0, r1) (the product's per-part backward launches)."""
     q, k, v, do = (_as3(x).astype(dtype) for x in (q, k, v, do))
     c_q, hq, _ = q.shape
     c_k, hkv, _ = k.shape
@@ -454,6 +456,10 @@ def block_backward(q, k, v, do, lse, dsum, kind: int, softmax_scale: float, dtyp
     if kind == FULLY_MASKED:
         return dq, dk, dv
     allowed = allowed_block(kind, 0, c_q, 0, c_k)
+    if key_rows is not None:
+        keep = np.zeros(c_k, dtype=bool)
+        keep[key_rows[0]:key_rows[1]] = True
+        allowed = allowed & keep[None, :]
     for h in range(hq):
         g = h // group
         s = (q[:, h] @ k[:, g].T) * dtype(softmax_scale)

@@ -27,6 +27,8 @@ SIGNATURES = {
     "sa_bwd_preprocess": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _I32, _P]),
     "sa_bwd_block": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32,
                                     _F32, _I32, _P]),
+    "sa_bwd_block_range": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32,
+                                          _I32, _F32, _I32, _I32, _I32, _P]),
     "sa_bwd_block_final": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32,
                                           _I32, _F32, _I32, _P]),
     "sa_cast_f32_bf16": (ctypes.c_int, [_P, _P, _I64, _P]),

@@ -171,6 +171,28 @@ int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, 
                     softmax_scale, mask_kind, static_cast<cudaStream_t>(stream));
 }
 
+int sa_bwd_block_range(const void* q, const void* k, const void* v, const void* dout,
+                       const float* lse, const float* dsum, float* dq_acc, float* dk_acc,
+                       float* dv_acc, int64_t c, int32_t hq, int32_t hkv, int32_t d,
+                       float softmax_scale, int32_t mask_kind, int32_t key_row_begin,
+                       int32_t key_row_end, void* stream) {
+  if (int r = check_heads(c, hq, hkv, d)) return r;
+  if (!q || !k || !v || !dout || !lse || !dsum || !dq_acc || !dk_acc || !dv_acc)
+    return fail_arg("null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq_acc) ||
+      !aligned16(dk_acc) || !aligned16(dv_acc))
+    return fail_arg("q/k/v/dout and the accumulators must be 16B aligned");
+  if (mask_kind < 0 || mask_kind > 3) return fail_arg("bad mask kind");
+  if (!(softmax_scale > 0.f)) return fail_arg("softmax_scale must be > 0");
+  if (key_row_begin < 0 || key_row_end > c || key_row_begin > key_row_end ||
+      key_row_begin % 128 || (key_row_end % 128 && key_row_end != c))
+    return fail_arg("key rows must be a 128-aligned sub-range of [0, c)");
+  if (mask_kind == SA_MASK_FULLY_MASKED || key_row_begin == key_row_end) return 0;
+  return launch_bwd(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, c, hq, hkv, d,
+                    softmax_scale, mask_kind, static_cast<cudaStream_t>(stream), nullptr,
+                    nullptr, key_row_begin / 128, (key_row_end + 127) / 128);
+}
+
 int sa_bwd_block_final(const void* q, const void* k, const void* v, const void* dout,
                        const float* lse, const float* dsum, float* dq_acc, void* dk, void* dv,
                        int64_t c, int32_t hq, int32_t hkv, int32_t d, float softmax_scale,

@@ -54,6 +54,7 @@ struct BwdParams {
   __nv_bfloat16* dk_out;
   __nv_bfloat16* dv_out;
   int c, hq, hkv, n_t;
+  int j_begin, n_j;  // key tiles [j_begin, j_begin + n_j) of the block (a part of it)
   float scale, scale_log2;
   int kind;
   int debug;         // perf experiments only: bit0 = skip the dQ reduction
@@ -132,8 +133,8 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
   // Head-major order: the ~148 concurrent CTAs share one kv head, so that head's Q / dO
   // and its dq_acc rows (the reduce-add target) stay L2-resident.  Within a head, small j
   // (most query tiles) first (LPT).
-  const int g = blockIdx.x / p.n_t;
-  const int j = blockIdx.x % p.n_t;
+  const int g = blockIdx.x / p.n_j;
+  const int j = p.j_begin + blockIdx.x % p.n_j;
   const int group = p.hq / p.hkv;
   const bool causal = p.kind != SA_MASK_FULLY_UNMASKED;
   const int i0 = causal ? j : 0;
@@ -520,7 +521,7 @@ int launch_bwd_d(BwdParams& prm, cudaStream_t st) {
   const int smem = BwdSmem<D>::kAlloc;
   static unsigned long long attr_devices = 0;
   if (int r = set_smem_attr_once(bwd_kernel<D>, smem, &attr_devices)) return r;
-  bwd_kernel<D><<<prm.n_t * prm.hkv, 512, smem, st>>>(prm);
+  bwd_kernel<D><<<prm.n_j * prm.hkv, 512, smem, st>>>(prm);
   return check_launch("bwd_kernel");
 }
 
@@ -529,7 +530,7 @@ int launch_bwd_d(BwdParams& prm, cudaStream_t st) {
 int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                const float* dsum, float* dq, float* dk, float* dv, int64_t c, int32_t hq,
                int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st,
-               void* dk_out, void* dv_out) {
+               void* dk_out, void* dv_out, int32_t kv_tile_begin, int32_t kv_tile_end) {
   BwdParams prm;
   prm.dk_out = static_cast<__nv_bfloat16*>(dk_out);
   prm.dv_out = static_cast<__nv_bfloat16*>(dv_out);
@@ -548,6 +549,9 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   prm.hq = hq;
   prm.hkv = hkv;
   prm.n_t = static_cast<int>((c + 127) / 128);
+  prm.j_begin = kv_tile_begin;
+  prm.n_j = (kv_tile_end < 0 ? prm.n_t : kv_tile_end) - kv_tile_begin;
+  if (prm.n_j <= 0) return 0;
   prm.scale = scale;
   prm.scale_log2 = scale * kLog2e;
   prm.kind = kind;

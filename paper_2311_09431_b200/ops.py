@@ -88,7 +88,9 @@ def bwd_preprocess(out, dout, dsum, dq_acc):
 
 
 def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: float,
-              mask_kind: int):
+              mask_kind: int, key_rows=None):
+    """K5: one ring step of the backward (accumulates into dq_acc / dk_acc / dv_acc);
+    ``key_rows=(r0, r1)`` restricts it to those held-stripe keys (sa_bwd_block_range)."""
     for n, t in (("q", q), ("k", k), ("v", v), ("dout", dout)):
         _need_cuda(n, t, torch.bfloat16)
     for n, t in (("lse", lse), ("dsum", dsum), ("dq_acc", dq_acc), ("dk_acc", dk_acc),
@@ -97,10 +99,17 @@ def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: f
     c, hq, d = q.shape
     hkv = k.shape[1]
     with _on(q):
-        _lib.check(_lib.lib().sa_bwd_block(
-            q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(), dsum.data_ptr(),
-            dq_acc.data_ptr(), dk_acc.data_ptr(), dv_acc.data_ptr(), c, hq, hkv, d,
-            float(softmax_scale), int(mask_kind), _stream(q)), "sa_bwd_block")
+        if key_rows is None:
+            _lib.check(_lib.lib().sa_bwd_block(
+                q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                dsum.data_ptr(), dq_acc.data_ptr(), dk_acc.data_ptr(), dv_acc.data_ptr(), c, hq,
+                hkv, d, float(softmax_scale), int(mask_kind), _stream(q)), "sa_bwd_block")
+        else:
+            _lib.check(_lib.lib().sa_bwd_block_range(
+                q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                dsum.data_ptr(), dq_acc.data_ptr(), dk_acc.data_ptr(), dv_acc.data_ptr(), c, hq,
+                hkv, d, float(softmax_scale), int(mask_kind), int(key_rows[0]),
+                int(key_rows[1]), _stream(q)), "sa_bwd_block_range")
 
 
 def bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, softmax_scale: float,

@@ -40,8 +40,10 @@ class BlockOps:
     def bwd_preprocess(self, out, dout, dsum, dq_acc):
         self._ops.bwd_preprocess(out, dout, dsum, dq_acc)
 
-    def bwd_block(self, q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind):
-        self._ops.bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind)
+    def bwd_block(self, q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind,
+                  key_rows=None):
+        self._ops.bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind,
+                            key_rows)
 
     def bwd_block_final(self, q, k, v, dout, lse, dsum, dq_acc, dk, dv, scale, kind):
         """Single-step backward: bf16 dK / dV written directly (no accumulators / casts)."""
@@ -113,6 +115,40 @@ class _Streams:
     def compute_after_comm(self):
         if self.cuda:
             self.compute.wait_stream(self.comm)
+
+    def _event(self, stream):
+        if not self.cuda:
+            return None
+        e = torch.cuda.Event()
+        e.record(stream)
+        return e
+
+    def compute_event(self):
+        return self._event(self.compute) if self.cuda else None
+
+    def comm_event(self):
+        return self._event(self.comm) if self.cuda else None
+
+    def compute_waits(self, ev):
+        if ev is not None:
+            self.compute.wait_event(ev)
+
+    def comm_waits(self, ev):
+        if ev is not None:
+            self.comm.wait_event(ev)
+
+
+def kv_parts(c: int, tile: int = 128) -> list:
+    """Row ranges of the held stripe's keys, in launch order, for the backward's
+    pipelined dK/dV hop: the upper half first (cheapest per row under a causal mask), then
+    the next quarter, the lowest quarter last, so the exposed hop is a quarter of the rows.
+    Blocks of fewer than 4 key tiles run in one part."""
+    nt = -(-c // tile)
+    if nt < 4:
+        return [(0, c)]
+    b1, b2 = nt // 4, nt // 2
+    rows = lambda t: min(c, t * tile)
+    return [(rows(b2), c), (rows(b1), rows(b2)), (0, rows(b1))]
 
 
 class Workspace:
@@ -286,34 +322,48 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
         cur = (k, v)
         dcur = (dk_acc, dv_acc)
         dspare = dkv_bufs[0]
+        # the block runs in parts over the held stripe's keys; each part's dK/dV rows hop
+        # to the next rank while the later parts compute (the last, smallest part's hop is
+        # the only one between rounds)
+        parts = kv_parts(c)
+        arrived = [None] * len(parts)  # comm-stream events: part p of dcur has arrived
         for i in range(world):
             held = (rank - i) % world
             pending = None
             nxt = kv_bufs[i % 2]
+            kv_ready = None
             if i < world - 1:
-                st.comm_after_compute()
+                st.comm_after_compute()  # nxt's previous reader (round i-1) has finished
                 with st.on_comm():
                     pending = comm.exchange(list(cur), list(nxt))
+                    for w in pending:
+                        w.wait()
+                kv_ready = st.comm_event()
             kind = masks.block_mask(layout, rank, held, world)
             timer.start()
-            bops.bwd_block(q, cur[0], cur[1], dout, lse, dsum, dq_acc, dcur[0], dcur[1],
-                           softmax_scale, kind)
+            sent = [None] * len(parts)
+            for pi, (r0, r1) in enumerate(parts):
+                st.compute_waits(arrived[pi])  # this part's accumulator rows are here
+                bops.bwd_block(q, cur[0], cur[1], dout, lse, dsum, dq_acc, dcur[0], dcur[1],
+                               softmax_scale, kind, key_rows=(r0, r1))
+                done = st.compute_event()
+                with st.on_comm():
+                    st.comm_waits(done)
+                    works = comm.exchange([dcur[0][r0:r1], dcur[1][r0:r1]],
+                                          [dspare[0][r0:r1], dspare[1][r0:r1]])
+                    for w in works:
+                        w.wait()
+                sent[pi] = st.comm_event()
             timer.stop()
             if stats is not None:
                 stats.rounds.append(StepRecord(i, held, int(kind)))
-            # dK/dV of the held stripe move on after this round's compute (N hops total)
-            st.comm_after_compute()
-            with st.on_comm():
-                dpend = comm.exchange(list(dcur), list(dspare))
-                for w in dpend:
-                    w.wait()
-                if pending is not None:
-                    for w in pending:
-                        w.wait()
-            st.compute_after_comm()
+            arrived = sent
             dcur, dspare = dspare, dcur
+            st.compute_waits(kv_ready)
             if pending is not None:
                 cur = nxt
+        for ev in arrived:  # the accumulators are home after the N-th hop
+            st.compute_waits(ev)
         dk_acc, dv_acc = dcur
     if stats is not None:
         timer.fill(stats.rounds)

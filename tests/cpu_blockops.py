@@ -46,10 +46,11 @@ class OracleBlockOps:
         dsum.copy_(torch.tensor(np.einsum("shd,shd->hs", _np(dout), _np(out)), dtype=dsum.dtype))
         dq_acc.zero_()
 
-    def bwd_block(self, q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind):
+    def bwd_block(self, q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind,
+                  key_rows=None):
         self.calls.append(("bwd", int(kind)))
         dq, dk, dv = R.block_backward(_np(q), _np(k), _np(v), _np(dout), _np(lse), _np(dsum),
-                                      int(kind), scale)
+                                      int(kind), scale, key_rows=key_rows)
         dq_acc += torch.tensor(dq, dtype=dq_acc.dtype)
         dk_acc += torch.tensor(dk, dtype=dk_acc.dtype)
         dv_acc += torch.tensor(dv, dtype=dv_acc.dtype)

@@ -159,3 +159,28 @@ def test_final_mode_equals_accumulate_then_cast(ops, kind, c, hq, hkv, d):
     assert torch.equal(dk_b.view(torch.int16), dk_a.bfloat16().view(torch.int16))
     assert torch.equal(dv_b.view(torch.int16), dv_a.bfloat16().view(torch.int16))
     assert (dq_a - dq_b).abs().max().item() <= 1e-4 * max(1.0, dq_a.abs().max().item())
+
+
+@pytest.mark.parametrize("kind", [2, 3, 1])
+def test_key_range_parts_equal_whole_block(ops, kind):
+    """sa_bwd_block_range over the ring's key parts (ring.kv_parts) == one full launch:
+    dK / dV bit for bit (same CTA per key tile), dQ up to the reduce-add order."""
+    from paper_2311_09431_b200.ring import kv_parts
+    c, hq, hkv, d = 1000, 4, 2, 128
+    gen = torch.Generator(device="cuda").manual_seed(21 + kind)
+    q, do = (torch.randn(c, hq, d, device="cuda", generator=gen).bfloat16() for _ in range(2))
+    k, v = (torch.randn(c, hkv, d, device="cuda", generator=gen).bfloat16() for _ in range(2))
+    lse = (torch.randn(hq, c, device="cuda", generator=gen).abs() + 3.0).contiguous()
+    dsum = torch.randn(hq, c, device="cuda", generator=gen)
+    acc = lambda h: torch.zeros(c, h, d, device="cuda")
+    full = [acc(hq), acc(hkv), acc(hkv)]
+    ops.bwd_block(q, k, v, do, lse, dsum, *full, 0.09, kind)
+    parts = [acc(hq), acc(hkv), acc(hkv)]
+    assert len(kv_parts(c)) == 3
+    for r0, r1 in kv_parts(c):
+        ops.bwd_block(q, k, v, do, lse, dsum, *parts, 0.09, kind, key_rows=(r0, r1))
+    torch.cuda.synchronize()
+    assert torch.equal(full[1], parts[1]) and torch.equal(full[2], parts[2])
+    assert (full[0] - parts[0]).abs().max().item() <= 1e-4 * max(1.0, full[0].abs().max().item())
+    with pytest.raises(Exception):
+        ops.bwd_block(q, k, v, do, lse, dsum, *parts, 0.09, kind, key_rows=(100, 300))

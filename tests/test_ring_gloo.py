@@ -26,7 +26,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, layout, result_q):
+def _worker(rank, world, port, layout, result_q, c_rank=16):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -38,7 +38,7 @@ def _worker(rank, world, port, layout, result_q):
         from cpu_blockops import OracleBlockOps
         from paper_2311_09431_b200 import ring, telemetry
 
-        n, hq, hkv, d = 16 * world, 4, 2, 8
+        n, hq, hkv, d = c_rank * world, 4, 2, 8
         rng = np.random.default_rng(7)
         q, k, v, do = (rng.standard_normal(s) for s in ((n, hq, d), (n, hkv, d), (n, hkv, d),
                                                          (n, hq, d)))
@@ -72,13 +72,16 @@ def _worker(rank, world, port, layout, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world,c_rank", [(2, 16), (4, 16), (2, 512)])
 @pytest.mark.parametrize("layout", ["striped", "ring"])
-def test_ring_driver_over_gloo(world, layout):
+def test_ring_driver_over_gloo(world, c_rank, layout):
+    """c_rank 512: the backward runs each block in 3 key parts whose dK/dV rows hop
+    separately (ring.kv_parts)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, q, c_rank))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
