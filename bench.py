@@ -196,6 +196,7 @@ def main():
         def __init__(self):
             super().__init__()
             self.events = []  # (name, start, end)
+            self._open = None  # start event of a backward round run in key parts
 
         def _wrap(self, name, fn, *a):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -208,7 +209,20 @@ def main():
             self._wrap("fwd_block", super().fwd_block, *a)
 
         def bwd_block(self, *a, **kw):
-            self._wrap("bwd_block", lambda *x: super(TimedOps, self).bwd_block(*x, **kw), *a)
+            rows = kw.get("key_rows")
+            if rows is None:
+                self._wrap("bwd_block", super().bwd_block, *a)
+                return
+            # a round in key parts (ring.kv_parts, the lowest rows last): one entry per round
+            if self._open is None:
+                self._open = torch.cuda.Event(enable_timing=True)
+                self._open.record()
+            super().bwd_block(*a, **kw)
+            if rows[0] == 0:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                self.events.append(("bwd_block", self._open, e))
+                self._open = None
 
         def bwd_block_final(self, *a):  # the N = 1 backward (bf16 dK / dV out of the kernel)
             self._wrap("bwd_block", super().bwd_block_final, *a)
