@@ -138,6 +138,21 @@ def cpu_sample(budget_s: float = 8.0):
     return flops / dt / 1e12, dt, desc, threads
 
 
+def arm_config(args, world):
+    """The workload both arms report (the reference arm runs a bounded sample of it)."""
+    hq, d = args.heads, args.dim
+    hkv = args.kv_heads or hq
+    c = args.stripe
+    n_seq = c * world
+    workload = ("configs[1]: single-B200 causal fwd+bwd, seq 32768, 32 heads, d 128 "
+                "(block kernels, no ring)") if world == 1 else \
+        (f"striped ring fwd+bwd, seq {n_seq} ({c} tokens/rank), {hq} heads, d {d}")
+    return {"workload": workload, "seq": n_seq, "stripe_tokens_per_rank": c, "heads_q": hq,
+            "heads_kv": hkv, "d_head": d, "layout": "striped", "parallelism": f"sp{world}",
+            "l2": "inputs 1 GiB/rank > 126 MB L2, no flush",
+            "useful_flops_per_step": useful_flops(n_seq, hq, d)}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -153,8 +168,7 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": "CPU oracle port of the striped causal fwd+bwd hot path "
-                                   "(bounded sample of configs[1])"},
+            "config": arm_config(args, world),
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
                              "sample": desc},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
@@ -409,18 +423,12 @@ def main():
 
     exposed = max(0.0, ms - kern_ms)
     if rank == 0:
-        workload = ("configs[1]: single-B200 causal fwd+bwd, seq 32768, 32 heads, d 128 "
-                    "(block kernels, no ring)") if world == 1 else \
-            (f"striped ring fwd+bwd, seq {n_seq} ({c} tokens/rank), {hq} heads, d {d}")
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded normal bf16 q/k/v/dO)",
-            "config": {"workload": workload, "seq": n_seq, "stripe_tokens_per_rank": c,
-                       "heads_q": hq, "heads_kv": hkv, "d_head": d, "layout": "striped",
-                       "parallelism": f"sp{world}", "l2": "inputs 1 GiB/rank > 126 MB L2, no flush",
-                       "useful_flops_per_step": total},
+            "config": arm_config(args, world),
             "per_gpu_value": value / world,
             "gpu_launches": launches,
             "kernel_ms_per_step": {kname: sum(xs) / args.steps for kname, xs in per.items()},
