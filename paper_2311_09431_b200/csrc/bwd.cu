@@ -40,6 +40,9 @@ namespace {
 
 constexpr uint32_t kPanelBytes = 128 * 128;  // 128 rows x 128 B
 constexpr float kLog2e = 1.4426950408889634f;
+#ifndef SA_BWD_DP_PREFETCH
+#define SA_BWD_DP_PREFETCH 1  // both dP^T chunks loaded before the first wait
+#endif
 #ifndef SA_BWD_POLY
 #define SA_BWD_POLY 0  // quads of every 8 whose exp2 runs on the FMA-pipe polynomial
 #endif
@@ -212,6 +215,25 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
                         128 * i, pol_q);
         }
       }
+    } else if (warp == 3 && lane == 0 && p.trace && blockIdx.x == p.trace_cta) {
+      // perf experiments only: completion time of every MMA group, in issue order
+      // dV(it) S(it+1) dQ(it) dK(it) dP(it+1)
+      for (int it = 0; it < n_it && it < 16; it++) {
+        mbar_wait(&bar[B_DO_EMPTY], it & 1);
+        SA_TR(24);
+        if (it + 1 < n_it) {
+          mbar_wait(&bar[B_S_FULL], (it + 1) & 1);
+          SA_TR(25);
+        }
+        mbar_wait(&bar[B_DQ_FULL], it & 1);
+        SA_TR(26);
+        mbar_wait(&bar[B_Q_EMPTY + (it & 1)], (it >> 1) & 1);
+        SA_TR(27);
+        if (it + 1 < n_it) {
+          mbar_wait(&bar[B_DP_FULL], (it + 1) & 1);
+          SA_TR(28);
+        }
+      }
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer
       // The whole warp walks the schedule (descriptor words stay warp-uniform); one elected
@@ -380,11 +402,21 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       // dQ/dK(it-1) read dS^T: the commit after dK(it-1) (Q stage (it-1)&1's barrier)
       if (it > 0) mbar_wait(&bar[B_Q_EMPTY + ((it - 1) & 1)], ((it - 1) >> 1) & 1);
       if (tr) SA_TR(12);
+#if SA_BWD_DP_PREFETCH
+      uint32_t dr_all[64];  // both dP^T chunks in flight before the first wait
+      SA_TMEM_LD32(t_dpt + lane_off + half * 64, (dr_all + 0));
+      SA_TMEM_LD32(t_dpt + lane_off + half * 64 + 32, (dr_all + 32));
+      tmem_ld_wait();
+#endif
 #pragma unroll
       for (int ch = 0; ch < 2; ch++) {
+#if SA_BWD_DP_PREFETCH
+        const uint32_t* dr = dr_all + ch * 32;
+#else
         uint32_t dr[32];
         SA_TMEM_LD32(t_dpt + lane_off + half * 64 + ch * 32, dr);
         tmem_ld_wait();
+#endif
         uint32_t dk[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
@@ -575,7 +607,7 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
     const long long t0 = h[0];
     for (int it = 0; it < 16; it++) {
       fprintf(stderr, "it%2d", it);
-      for (int k = 0; k < 23; k++) fprintf(stderr, " %6lld", h[it * 32 + k] ? h[it * 32 + k] - t0 : -1);
+      for (int k = 0; k < 29; k++) fprintf(stderr, " %6lld", h[it * 32 + k] ? h[it * 32 + k] - t0 : -1);
       fprintf(stderr, "\n");
     }
   }
