@@ -399,8 +399,9 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       mbar_wait(&bar[B_DP_FULL], it & 1);
       if (tr) SA_TR(11);
       tc_fence_after();
-      // dQ/dK(it-1) read dS^T: the commit after dK(it-1) (Q stage (it-1)&1's barrier)
-      if (it > 0) mbar_wait(&bar[B_Q_EMPTY + ((it - 1) & 1)], ((it - 1) >> 1) & 1);
+      // dQ/dK(it-1) must have read dS^T before it is overwritten: implied by DP_FULL(it),
+      // whose commit was issued after dK(it-1) (a commit tracks ALL prior MMAs of the
+      // issuing thread), so no separate wait sits on the dS -> dQ -> dP critical cycle
       if (tr) SA_TR(12);
 #if SA_BWD_DP_PREFETCH
       uint32_t dr_all[64];  // both dP^T chunks in flight before the first wait
