@@ -122,16 +122,11 @@ int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
 int sa_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
                       int64_t height, void* stream);
 
-/* Test-only: exercises the tcgen05 / TMA operand layouts the kernels rely on, on one
- * 128x128x128 tile: s = a b^T, o = bf16(s) v, y = b^T v (a, b, v bf16 [128,128] row-major;
- * outputs fp32 [128,128]). */
-int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* o, float* y,
-                  void* stream);
-
-/* Test-only: the CTA-pair (tcgen05 cta_group::2) operand layouts: s = a b^T (a [256,128],
- * b [128,128]), o = bf16(s) v (v [128,128]), s2 = a b^T with A staged in TMEM. */
-int sa_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
-                  void* stream);
+/* Device<->device (or peer) copy of `bytes` bytes on `stream` (cudaMemcpyAsync with
+ * cudaMemcpyDefault: a copy engine, NVLink between peers).  The ring's copy-engine hop
+ * (ring.LocalComm, ipc.IpcComm) -- the reference's per-round message hand-off,
+ * simulator.py:211-215 -- issued without NCCL kernels on the SMs. */
+int sa_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -33,8 +33,7 @@ SIGNATURES = {
                                           _I32, _F32, _I32, _P]),
     "sa_cast_f32_bf16": (ctypes.c_int, [_P, _P, _I64, _P]),
     "sa_memcpy2d_async": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),
-    "sa_probe_umma": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
-    "sa_probe_pair": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "sa_memcpy_async": (ctypes.c_int, [_P, _P, _I64, _P]),
 }
 
 

@@ -65,6 +65,26 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     return out
 
 
+PROBE_SRC = os.path.join(ROOT, "tests", "csrc", "probe.cu")
+PROBE_OUT = os.path.join(ROOT, "tests", "csrc", "libsa_probe.so")
+
+
+def build_probe(force: bool = False) -> str:
+    """Test-only library (tcgen05 / TMA layout probes): tests/csrc/libsa_probe.so.  Kept
+    out of the product library; shares only the header-only device helpers."""
+    if not force and os.path.exists(PROBE_OUT) and \
+            os.path.getmtime(PROBE_OUT) > max(os.path.getmtime(PROBE_SRC),
+                                              os.path.getmtime(os.path.join(CSRC, "common.cuh"))):
+        return PROBE_OUT
+    tmp = PROBE_OUT + ".tmp"
+    cmd = [NVCC, *ARCH, *FLAGS, "-I" + CSRC, "-shared", PROBE_SRC, "-o", tmp]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed for probe.cu:\n{r.stdout}\n{r.stderr}")
+    os.replace(tmp, PROBE_OUT)
+    return PROBE_OUT
+
+
 if __name__ == "__main__":
     outs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
     print(build(force="--force" in sys.argv or bool(outs), verbose="-v" in sys.argv,

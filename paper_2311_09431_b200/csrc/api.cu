@@ -75,19 +75,6 @@ int make_tmap_rows_f32(CUtensorMap* map, const void* base, int64_t rows, int32_t
   return r == CUDA_SUCCESS ? 0 : fail_arg("cuTensorMapEncodeTiled(f32) failed");
 }
 
-int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int32_t box_rows) {
-  auto fn = encode_fn();
-  if (!fn) return fail_arg("cuTensorMapEncodeTiled unavailable");
-  cuuint64_t sizes[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), sizes,
-                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : fail_arg("cuTensorMapEncodeTiled(2d) failed");
-}
-
 static int check_heads(int64_t c, int32_t hq, int32_t hkv, int32_t d) {
   if (c < 1) return fail_arg("block length c must be >= 1");
   if (c > (int64_t(1) << 31) - 256) return fail_arg("block length too large");
@@ -237,16 +224,16 @@ int sa_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch
   return 0;
 }
 
-int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* o, float* y,
-                  void* stream) {
-  if (!a || !b || !v || !s || !o || !y) return fail_arg("null pointer");
-  return launch_probe(a, b, v, s, o, y, static_cast<cudaStream_t>(stream));
-}
-
-int sa_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
-                  void* stream) {
-  if (!a || !b || !v || !s || !o || !s2) return fail_arg("null pointer");
-  return launch_probe_pair(a, b, v, s, o, s2, static_cast<cudaStream_t>(stream));
+int sa_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  if (!dst || !src || bytes < 0) return fail_arg("bad copy arguments");
+  if (bytes == 0) return 0;
+  cudaError_t e = cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), cudaMemcpyDefault,
+                                  static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMemcpyAsync: ") + cudaGetErrorString(e));
+    return -static_cast<int>(e);
+  }
+  return 0;
 }
 
 }  // extern "C"

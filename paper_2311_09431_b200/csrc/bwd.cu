@@ -67,7 +67,7 @@ struct BwdParams {
 
 #define SA_TR(slot)                                                                     \
   do {                                                                                  \
-    if (p.trace && blockIdx.x == p.trace_cta && it < 16) p.trace[it * 32 + (slot)] = clock64(); \
+    if (SA_PERF_TRACE && p.trace && blockIdx.x == p.trace_cta && it < 16) p.trace[it * 32 + (slot)] = clock64(); \
   } while (0)
 
 template <int D>
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
                         128 * i, pol_q);
         }
       }
-    } else if (warp == 3 && lane == 0 && p.trace && blockIdx.x == p.trace_cta) {
+    } else if (SA_PERF_TRACE && warp == 3 && lane == 0 && p.trace && blockIdx.x == p.trace_cta) {
       // perf experiments only: completion time of every MMA group, in issue order
       // dV(it) S(it+1) dQ(it) dK(it) dP(it+1)
       for (int it = 0; it < n_it && it < 16; it++) {
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       if (tr) SA_TR(8);
       tc_fence_after();
       mbar_wait(&bar[B_LSE_FULL + s], (it >> 1) & 1);
-      if (p.debug & 4) {  // perf experiments only: no compute, just the hand-offs
+      if (SA_PERF_TRACE && (p.debug & 4)) {  // perf experiments only: no compute, just the hand-offs
         tc_fence_before();
         mbar_arrive(&bar[B_P_READY]);
         mbar_wait(&bar[B_DP_FULL], it & 1);
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       tc_fence_before();
       mbar_arrive(&bar[B_DQ_FREE]);
       if (leader) SA_TR(18);
-      if (p.debug & 1) continue;
+      if (SA_PERF_TRACE && (p.debug & 1)) continue;
 #pragma unroll
       for (int ch = 0; ch < kChunks; ch++) {
         const uint32_t buf = sbase + L::kStg + (ch & 1) * kPanelBytes;
@@ -503,7 +503,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (leader) {
-          if (!(p.debug & 8))  // perf experiments only: bit 3 stages dQ but skips the reduce
+          if (!(SA_PERF_TRACE && (p.debug & 8)))  // perf experiments only: bit 3 stages dQ but skips the reduce
             tma_reduce_add_3d(&p.tdq, smem + L::kStg + (ch & 1) * kPanelBytes, 32 * ch, h, 128 * i);
           bulk_commit();
         }
@@ -588,10 +588,12 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
   prm.scale = scale;
   prm.scale_log2 = scale * kLog2e;
   prm.kind = kind;
-  const char* dbg = getenv("SA_BWD_DEBUG");
-  prm.debug = dbg ? atoi(dbg) : 0;
+  prm.debug = 0;
   prm.trace = nullptr;
   prm.trace_cta = 0;
+#if SA_PERF_TRACE
+  const char* dbg = getenv("SA_BWD_DEBUG");
+  prm.debug = dbg ? atoi(dbg) : 0;
   static long long* trace_buf = nullptr;
   const char* tr = getenv("SA_BWD_TRACE");  // perf experiments: dump one CTA's timeline
   if (tr) {
@@ -600,7 +602,9 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
     prm.trace = trace_buf;
     prm.trace_cta = atoi(tr);
   }
+#endif
   int r = d == 128 ? launch_bwd_d<128>(prm, st) : launch_bwd_d<64>(prm, st);
+#if SA_PERF_TRACE
   if (tr && r == 0) {
     long long h[16 * 32];
     cudaStreamSynchronize(st);
@@ -612,6 +616,7 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
       fprintf(stderr, "\n");
     }
   }
+#endif
   return r;
 }
 

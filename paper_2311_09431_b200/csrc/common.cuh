@@ -16,6 +16,13 @@
 
 #define SA_DEV __device__ __forceinline__
 
+// Perf-experiment instrumentation (clock64 timelines, debug knobs read from the
+// environment).  OFF in the product build: the launch paths then read no environment,
+// allocate nothing and never synchronise.  Build with SA_NVCC_EXTRA=-DSA_PERF_TRACE=1.
+#ifndef SA_PERF_TRACE
+#define SA_PERF_TRACE 0
+#endif
+
 namespace sa {
 
 SA_DEV uint32_t smem_u32(const void* p) {
@@ -25,6 +32,11 @@ SA_DEV uint32_t smem_u32(const void* p) {
 SA_DEV uint32_t warp_id() { return threadIdx.x >> 5; }
 SA_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 
+// One lane of a fully active warp.  INVARIANT relied on by every MMA issuer: with the
+// full member mask elect.sync picks the same (lowest active) lane every time, so all of a
+// warp's tcgen05.mma / tcgen05.commit come from ONE thread -- a commit tracks only the
+// earlier tcgen05 ops of its own thread (bwd.cu's DP_FULL / KV_DONE commits depend on it).
+// Call only from warps whose 32 lanes are all active.
 SA_DEV bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

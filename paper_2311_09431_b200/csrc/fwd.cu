@@ -55,7 +55,7 @@ struct FwdParams {
 
 #define SA_TR(slot)                                                                     \
   do {                                                                                  \
-    if (p.trace && blockIdx.x == p.trace_cta && j < 16) p.trace[j * 32 + (slot)] = clock64(); \
+    if (SA_PERF_TRACE && p.trace && blockIdx.x == p.trace_cta && j < 16) p.trace[j * 32 + (slot)] = clock64(); \
   } while (0)
 
 template <int D>
@@ -408,7 +408,7 @@ int launch_fwd_d(FwdParams& prm, cudaStream_t st) {
 int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float* lse, void* out,
                int64_t c, int32_t hq, int32_t hkv, int32_t d, float scale, int32_t kind,
                int32_t first, int32_t last, int64_t* tiles, cudaStream_t st) {
-  if (fwd_pair_enabled(d) && !getenv("SA_FWD_TRACE"))
+  if (fwd_pair_enabled(d) && !(SA_PERF_TRACE && getenv("SA_FWD_TRACE")))
     return launch_fwd_pair(q, k, v, o_acc, lse, out, c, hq, hkv, scale, kind, first, last, tiles, st);
   FwdParams prm;
   if (int r = make_tmap_rows(&prm.tq, q, c, hq, d, 128)) return r;
@@ -428,6 +428,7 @@ int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float*
   prm.last = last;
   prm.trace = nullptr;
   prm.trace_cta = 0;
+#if SA_PERF_TRACE
   static long long* trace_buf = nullptr;
   const char* tr = getenv("SA_FWD_TRACE");  // perf experiments: dump one CTA's timeline
   if (tr) {
@@ -450,6 +451,7 @@ int launch_fwd(const void* q, const void* k, const void* v, float* o_acc, float*
     }
     return r;
   }
+#endif
   return d == 128 ? launch_fwd_d<128>(prm, st) : launch_fwd_d<64>(prm, st);
 }
 

@@ -70,7 +70,7 @@ struct PairParams {
 
 #define SA_TR(slot)                                                                       \
   do {                                                                                    \
-    if (p.trace && blockIdx.x == 0 && j < 16) p.trace[j * 32 + (slot)] = clock64();      \
+    if (SA_PERF_TRACE && p.trace && blockIdx.x == 0 && j < 16) p.trace[j * 32 + (slot)] = clock64();      \
   } while (0)
 
 struct Bars {
@@ -150,7 +150,7 @@ fwd_pair_kernel(const __grid_constant__ PairParams p) {
       // drain: the leader's last commits must land before this CTA may exit
       for (int j = max(0, n - kSt); j < n - 1; j++) mbar_wait(&bar.pv_done[j % kSt], (j / kSt) & 1);
       mbar_wait(&bar.o_final, 0);
-    } else if (warp == 3 - SA_PROD_WARP && rank == 0 && lane == 0 && p.trace && blockIdx.x == 0) {
+    } else if (warp == 3 - SA_PROD_WARP && rank == 0 && lane == 0 && SA_PERF_TRACE && p.trace && blockIdx.x == 0) {
       // perf experiments only: completion times of S(j) / PV(j) for the first 16 tiles
       for (int j = 0; j < 16 && j < n - 1; j++) {
         mbar_wait(&bar.s_full[j % kSBuf], (j / kSBuf) & 1);
@@ -406,7 +406,11 @@ fwd_pair_kernel(const __grid_constant__ PairParams p) {
 }  // namespace
 
 bool fwd_pair_enabled(int32_t d) {
+#if SA_PERF_TRACE
   static const bool off = getenv("SA_FWD_SINGLE") != nullptr;  // A/B against fwd.cu
+#else
+  constexpr bool off = false;
+#endif
   return d == 128 && !off;
 }
 
@@ -430,8 +434,13 @@ int launch_fwd_pair(const void* q, const void* k, const void* v, float* o_acc, f
   prm.first = first;
   prm.last = last;
   prm.trace = nullptr;
+#if SA_PERF_TRACE
   static long long* trace_buf = nullptr;
   const bool tr = getenv("SA_FWD_PAIR_TRACE") != nullptr;
+#else
+  constexpr bool tr = false;
+  long long* trace_buf = nullptr;
+#endif
   if (tr) {
     if (!trace_buf) cudaMalloc(&trace_buf, 32 * 32 * sizeof(long long));
     cudaMemsetAsync(trace_buf, 0, 32 * 32 * sizeof(long long), st);
@@ -440,6 +449,7 @@ int launch_fwd_pair(const void* q, const void* k, const void* v, float* o_acc, f
   static unsigned long long attr_devices = 0;
   if (int r = set_smem_attr_once(fwd_pair_kernel, kSmemBytes, &attr_devices)) return r;
   fwd_pair_kernel<<<2 * prm.n_pair * hq, 384, kSmemBytes, st>>>(prm);
+#if SA_PERF_TRACE
   if (tr) {
     long long hbuf[32 * 32];
     cudaStreamSynchronize(st);
@@ -452,6 +462,7 @@ int launch_fwd_pair(const void* q, const void* k, const void* v, float* o_acc, f
       fprintf(stderr, "\n");
     }
   }
+#endif
   return check_launch("fwd_pair_kernel");
 }
 

@@ -5,6 +5,10 @@
 #include <cstdint>
 #include <string>
 
+#ifndef SA_PERF_TRACE
+#define SA_PERF_TRACE 0  // see common.cuh
+#endif
+
 namespace sa {
 
 void set_error(const std::string& msg);
@@ -37,15 +41,9 @@ int make_tmap_rows(CUtensorMap* map, const void* base, int64_t rows, int32_t hea
 // fp32 [rows, heads, dim] map, box (32 x 1 x box_rows), SW128 (accumulator TMA reduce-add).
 int make_tmap_rows_f32(CUtensorMap* map, const void* base, int64_t rows, int32_t heads,
                        int32_t dim, int32_t box_rows);
-// 2-D bf16 [rows, cols] map, box (64 x box_rows), SW128 (probe kernel).
-int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int32_t box_rows);
 
 int launch_permute(const void* src, void* dst, int64_t n_seq, int32_t n_dev, int64_t row_bytes,
                    int32_t scheme, int32_t direction, int32_t device, cudaStream_t st);
-int launch_probe(const void* a, const void* b, const void* v, float* s, float* o, float* y,
-                 cudaStream_t st);
-int launch_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
-                      cudaStream_t st);
 bool fwd_pair_enabled(int32_t d);
 int launch_fwd_pair(const void* q, const void* k, const void* v, float* o_acc, float* lse,
                     void* out, int64_t c, int32_t hq, int32_t hkv, float scale, int32_t kind,

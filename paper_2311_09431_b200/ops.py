@@ -138,28 +138,3 @@ def cast_f32_bf16(src: torch.Tensor, dst: torch.Tensor) -> torch.Tensor:
         _lib.check(_lib.lib().sa_cast_f32_bf16(src.data_ptr(), dst.data_ptr(), src.numel(),
                                                _stream(src)), "sa_cast_f32_bf16")
     return dst
-
-
-def probe_umma(a, b, v):
-    """Test-only: returns (s, o, y) = (a b^T, bf16(s) v, b^T v) computed with tcgen05."""
-    for n, t in (("a", a), ("b", b), ("v", v)):
-        _need_cuda(n, t, torch.bfloat16)
-        if t.shape != (128, 128):
-            raise ValueError("probe tiles are 128x128")
-    s, o, y = (torch.empty(128, 128, device=a.device, dtype=torch.float32) for _ in range(3))
-    with _on(a):
-        _lib.check(_lib.lib().sa_probe_umma(a.data_ptr(), b.data_ptr(), v.data_ptr(), s.data_ptr(),
-                                            o.data_ptr(), y.data_ptr(), _stream(a)), "sa_probe_umma")
-    return s, o, y
-
-
-def probe_pair(a, b, v):
-    """Test-only: CTA-pair (cta_group::2) layouts. a [256,128], b [128,128], v [128,128] bf16.
-    Returns (s, o, s2) = (a b^T, bf16(s) v, a b^T with A staged in TMEM)."""
-    for n, t in (("a", a), ("b", b), ("v", v)):
-        _need_cuda(n, t, torch.bfloat16)
-    s, o, s2 = (torch.empty(256, 128, device=a.device, dtype=torch.float32) for _ in range(3))
-    with _on(a):
-        _lib.check(_lib.lib().sa_probe_pair(a.data_ptr(), b.data_ptr(), v.data_ptr(), s.data_ptr(),
-                                            o.data_ptr(), s2.data_ptr(), _stream(a)), "sa_probe_pair")
-    return s, o, s2

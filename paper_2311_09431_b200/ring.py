@@ -5,26 +5,43 @@ stripe resident, runs the block op against the key/value stripe it holds -- held
 ``(j - i) mod N`` at round i (simulator.py:115-117) -- then forwards that stripe to
 ``j + 1`` and receives from ``j - 1``.  The reference swaps Python references
 (_run_serial, 194-197) or passes them through ordered queues (_run_threads, 211-215);
-here the hop is a point-to-point transfer over NVLink issued on a side stream and
-double-buffered, so round i+1's K/V arrive while round i computes.
+here the hop is a point-to-point transfer issued on a side stream and double-buffered,
+so round i+1's K/V arrive while round i computes.
+
+The hop itself is pluggable (``Comm``):
+
+* ``NcclComm``  -- torch.distributed P2P (NCCL over NVLink between processes; gloo for
+  CPU tensors in the host-logic tests);
+* ``LocalComm`` -- ranks as threads of ONE process (several GPUs of a node, or virtual
+  ranks sharing one GPU): a copy-engine ``cudaMemcpyAsync`` into the next rank's receive
+  buffer, ordered by CUDA events handed over through per-rank FIFO inboxes -- the
+  reference's threaded executor (one inbox per device written only by its predecessor,
+  30 s stall timeout, simulator.py:201-234) with device buffers instead of references;
+* ``IpcComm`` (``ipc.py``) -- one process per GPU, the same protocol over CUDA IPC
+  memory / event handles: copy engines instead of NCCL kernels on the SMs.
 
 Backward (no reference counterpart): fp32 dK/dV accumulators ride with their K/V
-stripe and arrive home after N hops; dQ accumulates locally.
+stripe and arrive home after N hops; dQ accumulates locally.  Each round runs in three
+key parts (``kv_parts``) and each part's dK/dV rows leave as soon as that part retires.
 
-Block ops are pluggable (``BlockOps``): the default is the CUDA library
-(``ops.py``); CPU tests inject an oracle-backed implementation to test this host logic
-over ``gloo`` without a GPU.
+Block ops are pluggable (``BlockOps``): the default is the CUDA library (``ops.py``);
+CPU tests inject an oracle-backed implementation to test this host logic over ``gloo``
+or ``LocalComm`` threads without a GPU.
 """
 
 from __future__ import annotations
 
 import contextlib
+import queue
+import threading
 from dataclasses import dataclass, field
 
 import torch
 import torch.distributed as dist
 
 from . import masks
+
+STALL_TIMEOUT_S = 30.0  # simulator.py:40 (ring channel stalled)
 
 
 class BlockOps:
@@ -64,22 +81,50 @@ class StepRecord:
 
 
 @dataclass
+class HopRecord:
+    """One ring hop on a side stream: what moved, how many bytes, its CUDA-event time
+    (from the hop's issue on the comm stream to its completion, waits included)."""
+    round: int
+    what: str  # "kv" | "dkv"
+    nbytes: int
+    ms: float = 0.0
+
+
+@dataclass
 class RingStats:
     rank: int
     rounds: list = field(default_factory=list)
+    hops: list = field(default_factory=list)
 
 
-class _Comm:
-    """Point-to-point neighbour exchange for one ring hop (torch.distributed P2P)."""
+# ----------------------------------------------------------------------------- comms
+class Comm:
+    """Neighbour exchange of one ring hop.  ``exchange(send, recv)``: ``send[i]`` goes to
+    the next rank's ``recv[i]`` and ``recv[i]`` is filled from the previous rank's
+    ``send[i]``.  For CUDA tensors the transfer is enqueued on the CURRENT stream (its
+    completion is stream-ordered, the call does not block on the GPU); CPU tensors are
+    exchanged before the call returns."""
 
-    def __init__(self, group):
+    rank: int = 0
+    world: int = 1
+    name: str = "comm"
+
+    def exchange(self, send, recv):  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class NcclComm(Comm):
+    """torch.distributed point-to-point (NCCL between GPUs, gloo for CPU tensors)."""
+
+    name = "nccl"
+
+    def __init__(self, group=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.next = dist.get_global_rank(group, (self.rank + 1) % self.world) if group is not None \
-            else (self.rank + 1) % self.world
-        self.prev = dist.get_global_rank(group, (self.rank - 1) % self.world) if group is not None \
-            else (self.rank - 1) % self.world
+        glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+        self.next = glob((self.rank + 1) % self.world)
+        self.prev = glob((self.rank - 1) % self.world)
 
     def exchange(self, send, recv):
         ops = []
@@ -89,53 +134,231 @@ class _Comm:
         # even ranks send first, odd ranks receive first (deadlock-free on any backend)
         if self.rank % 2:
             ops = [o for pair in zip(ops[1::2], ops[0::2]) for o in pair]
-        return dist.batch_isend_irecv(ops)
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()  # NCCL: the current stream waits; gloo: the host waits
 
 
-def _is_cuda(t):
-    return t.is_cuda
+class LocalRing:
+    """Shared state of ``world`` ranks running as threads of one process.
+
+    Two FIFO inboxes per rank, each written only by one neighbour (the ordered P2P
+    channels of simulator.py:201-234): ``ready[j]`` holds the receive buffers rank j+1
+    offers for rank j's next send, ``data[j]`` the completion events of the sends into
+    rank j's buffers."""
+
+    def __init__(self, world: int, timeout: float = STALL_TIMEOUT_S):
+        if world < 1:
+            raise ValueError("world must be >= 1")
+        self.world = world
+        self.timeout = timeout
+        self.ready = [queue.Queue() for _ in range(world)]
+        self.data = [queue.Queue() for _ in range(world)]
+        self.aborted = threading.Event()
+        self._shared = {}
+        self._barrier = threading.Barrier(world)
+
+    def comm(self, rank: int) -> "LocalComm":
+        return LocalComm(self, rank)
+
+    def abort(self):
+        self.aborted.set()
+        self._barrier.abort()
+
+    def get(self, q: queue.Queue, rank: int):
+        waited = 0.0
+        while True:
+            if self.aborted.is_set():
+                raise RuntimeError(f"ring aborted (rank {rank})")
+            try:
+                return q.get(timeout=0.25)
+            except queue.Empty:
+                waited += 0.25
+                if waited >= self.timeout:
+                    self.abort()
+                    raise RuntimeError(f"ring channel stalled (rank {rank})")
+
+    def all_gather(self, rank: int, key, value) -> list:
+        """Every rank's ``value`` for ``key`` (host objects; blocks until all posted)."""
+        slot = self._shared.setdefault(key, [None] * self.world)
+        slot[rank] = value
+        self._barrier.wait(timeout=self.timeout)
+        out = list(slot)
+        self._barrier.wait(timeout=self.timeout)
+        if rank == 0:
+            self._shared.pop(key, None)
+        return out
+
+
+def _record(ref: torch.Tensor):
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(ref.device))
+    return ev
+
+
+def _copy_async(dst: torch.Tensor, src: torch.Tensor):
+    """Copy-engine copy on the current stream (peer copy over NVLink across devices)."""
+    from . import _lib
+    if dst.numel() != src.numel() or dst.dtype != src.dtype:
+        raise ValueError("hop buffers differ in size or dtype")
+    if not (dst.is_contiguous() and src.is_contiguous()):
+        raise ValueError("hop buffers must be contiguous")
+    nbytes = src.numel() * src.element_size()
+    if nbytes == 0:
+        return
+    st = torch.cuda.current_stream(src.device).cuda_stream
+    _lib.check(_lib.lib().sa_memcpy_async(dst.data_ptr(), src.data_ptr(), nbytes, st),
+               "sa_memcpy_async")
+
+
+class LocalComm(Comm):
+    """One rank of a ``LocalRing`` (see there).  Per exchange:
+    1. offer my receive buffers to the previous rank, with an event marking the point on
+       my stream after which they may be overwritten;
+    2. take the next rank's offer, make my stream wait for its event, copy my send
+       buffers into its receive buffers (copy engine), record a completion event and
+       post it to the next rank;
+    3. take the previous rank's completion event and make my stream wait for it.
+    Every event is recorded before it is handed over, so no wait can precede its record
+    (the enqueued work stays acyclic)."""
+
+    name = "local"
+
+    def __init__(self, ring: LocalRing, rank: int):
+        self.ring = ring
+        self.rank = rank
+        self.world = ring.world
+        self.next = (rank + 1) % ring.world
+        self.prev = (rank - 1) % ring.world
+
+    def exchange(self, send, recv):
+        r = self.ring
+        cuda = recv[0].is_cuda
+        r.ready[self.prev].put((list(recv), _record(recv[0]) if cuda else None))
+        dst, free = r.get(r.ready[self.rank], self.rank)
+        if len(dst) != len(send):
+            raise RuntimeError("ring peers disagree on the hop's tensors")
+        if cuda:
+            torch.cuda.current_stream(send[0].device).wait_event(free)
+            for s, d in zip(send, dst):
+                _copy_async(d, s)
+            done = _record(send[0])
+        else:
+            for s, d in zip(send, dst):
+                d.copy_(s)
+            done = None
+        r.data[self.next].put(done)
+        ev = r.get(r.data[self.rank], self.rank)
+        if cuda and ev is not None:
+            torch.cuda.current_stream(recv[0].device).wait_event(ev)
+
+
+def run_local_ring(world: int, fn, devices=None, timeout: float = STALL_TIMEOUT_S):
+    """Run ``fn(rank, comm)`` for every rank as a thread of this process (LocalComm).
+
+    ``devices``: the CUDA device of each rank (default: none -- CPU, or whatever ``fn``
+    uses).  Each CUDA rank gets its own compute stream.  Returns the per-rank results;
+    the first exception of any rank is re-raised after all threads joined
+    (simulator.py:221-233)."""
+    ring = LocalRing(world, timeout)
+    results = [None] * world
+    errors = []
+
+    def worker(j):
+        try:
+            if devices is not None:
+                dev = torch.device(devices[j])
+                with torch.cuda.device(dev), torch.cuda.stream(torch.cuda.Stream(dev)):
+                    results[j] = fn(j, ring.comm(j))
+                    torch.cuda.current_stream(dev).synchronize()
+            else:
+                results[j] = fn(j, ring.comm(j))
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            errors.append((j, e))
+            ring.abort()
+
+    threads = [threading.Thread(target=worker, args=(j,), daemon=True) for j in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        errors.sort(key=lambda x: isinstance(x[1], RuntimeError) and "aborted" in str(x[1]))
+        raise errors[0][1]
+    return results
+
+
+def default_comm(group=None):
+    """The comm of ``group`` under torch.distributed, or None (one rank)."""
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        return NcclComm(group)
+    return None
+
+
+# ----------------------------------------------------------------------------- streams
+_tls = threading.local()
+
+
+def _side_streams(device: torch.device):
+    """Two persistent side streams per (thread, device): K/V hops and dK/dV hops.  Created
+    once (never from the shared pool on each call, which could alias other users'
+    streams such as the host API's copy streams)."""
+    cache = getattr(_tls, "streams", None)
+    if cache is None:
+        cache = _tls.streams = {}
+    key = device.index
+    if key not in cache:
+        cache[key] = (torch.cuda.Stream(device=device), torch.cuda.Stream(device=device))
+    return cache[key]
 
 
 class _Streams:
-    """Compute on the current stream, hops on a side stream (CUDA); no-ops on CPU."""
+    """Compute on the current stream, hops on side streams (CUDA); no-ops on CPU."""
 
     def __init__(self, ref: torch.Tensor):
-        self.cuda = _is_cuda(ref)
+        self.cuda = ref.is_cuda
+        self.compute = self.kv = self.dkv = None
         if self.cuda:
             self.compute = torch.cuda.current_stream(ref.device)
-            self.comm = torch.cuda.Stream(device=ref.device)
+            self.kv, self.dkv = _side_streams(ref.device)
 
-    def on_comm(self):
-        return torch.cuda.stream(self.comm) if self.cuda else contextlib.nullcontext()
+    def on(self, stream):
+        return torch.cuda.stream(stream) if self.cuda else contextlib.nullcontext()
 
-    def comm_after_compute(self):
-        if self.cuda:
-            self.comm.wait_stream(self.compute)
-
-    def compute_after_comm(self):
-        if self.cuda:
-            self.compute.wait_stream(self.comm)
-
-    def _event(self, stream):
+    def event(self, stream, timing=False):
         if not self.cuda:
             return None
-        e = torch.cuda.Event()
+        e = torch.cuda.Event(enable_timing=timing)
         e.record(stream)
         return e
 
-    def compute_event(self):
-        return self._event(self.compute) if self.cuda else None
+    def wait(self, stream, ev):
+        if ev is not None and self.cuda:
+            stream.wait_event(ev)
 
-    def comm_event(self):
-        return self._event(self.comm) if self.cuda else None
 
-    def compute_waits(self, ev):
-        if ev is not None:
-            self.compute.wait_event(ev)
+class _HopTimer:
+    def __init__(self, st: _Streams, stats):
+        self.on = stats is not None and st.cuda
+        self.stats = stats
+        self.st = st
+        self.pending = []
 
-    def comm_waits(self, ev):
-        if ev is not None:
-            self.comm.wait_event(ev)
+    def start(self, stream):
+        return self.st.event(stream, timing=True) if self.on else None
+
+    def stop(self, stream, start, rnd, what, tensors):
+        if self.on:
+            nbytes = sum(t.numel() * t.element_size() for t in tensors)
+            self.pending.append((HopRecord(rnd, what, nbytes), start,
+                                 self.st.event(stream, timing=True)))
+
+    def fill(self):
+        if not self.on:
+            return
+        for rec, a, b in self.pending:
+            b.synchronize()
+            rec.ms = a.elapsed_time(b)
+            self.stats.hops.append(rec)
 
 
 def kv_parts(c: int, tile: int = 128) -> list:
@@ -186,7 +409,7 @@ class _StepTimer:
     """CUDA-event time of each round's block kernel on the compute stream (telemetry)."""
 
     def __init__(self, ref: torch.Tensor, enabled: bool):
-        self.on = enabled and _is_cuda(ref)
+        self.on = enabled and ref.is_cuda
         self.events = []
 
     def start(self):
@@ -210,16 +433,27 @@ class _StepTimer:
             rec.compute_ms = a.elapsed_time(b)
 
 
+def _rank_world(group, comm):
+    if comm is not None:
+        return comm.rank, comm.world
+    if dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
 def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale: float,
                  block_ops: BlockOps | None = None, stats: RingStats | None = None,
-                 count_tiles: bool = False, workspace: Workspace | None = None):
+                 count_tiles: bool = False, workspace: Workspace | None = None,
+                 comm: Comm | None = None):
     """Forward for this rank's stripe.  q [c,Hq,D], k/v [c,Hkv,D] (bf16 on GPU).
 
-    Returns (out [c,Hq,D] bf16, lse [Hq,c] fp32) in local (permuted) order, like
-    run_schedule's outputs (simulator.py:237-277)."""
+    ``comm``: the hop backend (default: NCCL P2P over ``group`` when torch.distributed
+    runs with more than one rank).  Returns (out [c,Hq,D] bf16, lse [Hq,c] fp32) in
+    local (permuted) order, like run_schedule's outputs (simulator.py:237-277)."""
     bops = block_ops or BlockOps()
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if comm is None:
+        comm = default_comm(group)
+    rank, world = _rank_world(group, comm)
     c, hq, d = q.shape
     ws = workspace
     out = _alloc(ws, "out", (c, hq, d), q.dtype, q.device)
@@ -237,19 +471,23 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
                                            int(tiles.item()) if tiles is not None else 0))
             timer.fill(stats.rounds)
         return out, lse
-    comm = _Comm(group)
     st = _Streams(q)
+    hops = _HopTimer(st, stats)
     bufs = [(_alloc(ws, f"kbuf{b}", k.shape, k.dtype, k.device),
              _alloc(ws, f"vbuf{b}", v.shape, v.dtype, v.device)) for b in range(2)]
     cur = (k, v)
     for i in range(world):
         held = (rank - i) % world
-        pending = None
         nxt = bufs[i % 2]
+        kv_ready = None
         if i < world - 1:
-            st.comm_after_compute()  # nxt's previous reader (round i-1) has finished
-            with st.on_comm():
-                pending = comm.exchange(list(cur), list(nxt))
+            # nxt's previous reader (round i-1) has finished; cur is complete
+            st.wait(st.kv, st.event(st.compute))
+            with st.on(st.kv):
+                h0 = hops.start(st.kv)
+                comm.exchange(list(cur), list(nxt))
+                hops.stop(st.kv, h0, i, "kv", cur)
+            kv_ready = st.event(st.kv)
         kind = masks.block_mask(layout, rank, held, world)
         before = int(tiles.item()) if (tiles is not None and stats is not None) else 0
         timer.start()
@@ -259,28 +497,30 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
         if stats is not None:
             after = int(tiles.item()) if tiles is not None else 0
             stats.rounds.append(StepRecord(i, held, int(kind), after - before))
-        if pending is not None:
-            with st.on_comm():
-                for w in pending:
-                    w.wait()
-            st.compute_after_comm()
+        if i < world - 1:
+            st.wait(st.compute, kv_ready)
             cur = nxt
     if stats is not None:
         timer.fill(stats.rounds)
+        hops.fill()
     return out, lse
 
 
 def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped",
                   softmax_scale: float, block_ops: BlockOps | None = None,
-                  stats: RingStats | None = None, workspace: Workspace | None = None):
+                  stats: RingStats | None = None, workspace: Workspace | None = None,
+                  comm: Comm | None = None):
     """Backward for this rank's stripe -> (dq, dk, dv) bf16 in local order.
 
-    K/V hop one rank per round (prefetched on the side stream); the fp32 dK/dV
-    accumulators of the held stripe hop after each round's compute and are home
-    after N hops."""
+    Per round the held block runs in key parts (``kv_parts``); each part's fp32 dK/dV
+    rows hop to the next rank on the dK/dV stream as soon as the part retires, and the
+    next round's K/V hop is issued right after the first part's (so with NCCL, whose
+    P2P ops to one peer share an internal stream, it does not delay that hop).  The
+    accumulators are home after N hops."""
     bops = block_ops or BlockOps()
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if comm is None:
+        comm = default_comm(group)
+    rank, world = _rank_world(group, comm)
     c, hq, d = q.shape
     hkv = k.shape[1]
     dev = q.device
@@ -313,58 +553,56 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
         if stats is not None:
             stats.rounds.append(StepRecord(0, 0, int(kind)))
     else:
-        comm = _Comm(group)
         st = _Streams(q)
+        hops = _HopTimer(st, stats)
         kv_bufs = [(_alloc(ws, f"bkbuf{b}", k.shape, k.dtype, dev),
                     _alloc(ws, f"bvbuf{b}", v.shape, v.dtype, dev)) for b in range(2)]
-        dkv_bufs = [(_alloc(ws, "dk_spare", dk_acc.shape, torch.float32, dev),
-                     _alloc(ws, "dv_spare", dv_acc.shape, torch.float32, dev))]
+        dspare = (_alloc(ws, "dk_spare", dk_acc.shape, torch.float32, dev),
+                  _alloc(ws, "dv_spare", dv_acc.shape, torch.float32, dev))
         cur = (k, v)
         dcur = (dk_acc, dv_acc)
-        dspare = dkv_bufs[0]
-        # the block runs in parts over the held stripe's keys; each part's dK/dV rows hop
-        # to the next rank while the later parts compute (the last, smallest part's hop is
-        # the only one between rounds)
         parts = kv_parts(c)
-        arrived = [None] * len(parts)  # comm-stream events: part p of dcur has arrived
+        arrived = [None] * len(parts)  # dK/dV-stream events: part p of dcur has arrived
         for i in range(world):
             held = (rank - i) % world
-            pending = None
             nxt = kv_bufs[i % 2]
+            round_start = st.event(st.compute)  # round i-1's kernels (nxt's reader) done
             kv_ready = None
-            if i < world - 1:
-                st.comm_after_compute()  # nxt's previous reader (round i-1) has finished
-                with st.on_comm():
-                    pending = comm.exchange(list(cur), list(nxt))
-                    for w in pending:
-                        w.wait()
-                kv_ready = st.comm_event()
             kind = masks.block_mask(layout, rank, held, world)
             timer.start()
             sent = [None] * len(parts)
             for pi, (r0, r1) in enumerate(parts):
-                st.compute_waits(arrived[pi])  # this part's accumulator rows are here
+                st.wait(st.compute, arrived[pi])  # this part's accumulator rows are here
                 bops.bwd_block(q, cur[0], cur[1], dout, lse, dsum, dq_acc, dcur[0], dcur[1],
                                softmax_scale, kind, key_rows=(r0, r1))
-                done = st.compute_event()
-                with st.on_comm():
-                    st.comm_waits(done)
-                    works = comm.exchange([dcur[0][r0:r1], dcur[1][r0:r1]],
-                                          [dspare[0][r0:r1], dspare[1][r0:r1]])
-                    for w in works:
-                        w.wait()
-                sent[pi] = st.comm_event()
+                st.wait(st.dkv, st.event(st.compute))
+                with st.on(st.dkv):
+                    h0 = hops.start(st.dkv)
+                    part = [dcur[0][r0:r1], dcur[1][r0:r1]]
+                    comm.exchange(part, [dspare[0][r0:r1], dspare[1][r0:r1]])
+                    hops.stop(st.dkv, h0, i, "dkv", part)
+                sent[pi] = st.event(st.dkv)
+                if pi == 0 and i < world - 1:
+                    # the next round's K/V, behind the first part's dK/dV hop
+                    st.wait(st.kv, round_start)
+                    with st.on(st.kv):
+                        h0 = hops.start(st.kv)
+                        comm.exchange(list(cur), list(nxt))
+                        hops.stop(st.kv, h0, i, "kv", cur)
+                    kv_ready = st.event(st.kv)
             timer.stop()
             if stats is not None:
                 stats.rounds.append(StepRecord(i, held, int(kind)))
             arrived = sent
             dcur, dspare = dspare, dcur
-            st.compute_waits(kv_ready)
-            if pending is not None:
+            if i < world - 1:
+                st.wait(st.compute, kv_ready)
                 cur = nxt
         for ev in arrived:  # the accumulators are home after the N-th hop
-            st.compute_waits(ev)
+            st.wait(st.compute, ev)
         dk_acc, dv_acc = dcur
+        if stats is not None:
+            hops.fill()
     if stats is not None:
         timer.fill(stats.rounds)
     dq = _alloc(ws, "dq", q.shape, q.dtype, dev)
@@ -377,9 +615,11 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
 
 
 def virtual_ring_forward(qs, ks, vs, *, layout: str = "striped", softmax_scale: float,
-                         block_ops: BlockOps | None = None, count_tiles: bool = False):
+                         block_ops: BlockOps | None = None, count_tiles: bool = False,
+                         timings: list | None = None):
     """All N ranks' stripes on ONE device, rounds in order (the reference's serial
-    executor, simulator.py:189-198).  Same kernels and merge as the distributed path."""
+    executor, simulator.py:189-198).  Same kernels and merge as the distributed path.
+    ``timings`` (a list): receives (round, rank, start, end) CUDA events per block."""
     bops = block_ops or BlockOps()
     n = len(qs)
     c, hq, d = qs[0].shape
@@ -394,17 +634,37 @@ def virtual_ring_forward(qs, ks, vs, *, layout: str = "striped", softmax_scale: 
             held = (j - i) % n
             kind = masks.block_mask(layout, j, held, n)
             before = int(tiles.item()) if tiles is not None else 0
+            ev = _ev_pair(timings)
             bops.fwd_block(qs[j], ks[held], vs[held], accs[j], lses[j], outs[j], softmax_scale,
                            kind, i == 0, i == n - 1, tiles)
+            _ev_close(timings, ev, i, j)
             after = int(tiles.item()) if tiles is not None else 0
             stats[j].rounds.append(StepRecord(i, held, int(kind), after - before))
     return outs, lses, stats
 
 
+def _ev_pair(timings):
+    if timings is None:
+        return None
+    s = torch.cuda.Event(enable_timing=True)
+    s.record()
+    return s
+
+
+def _ev_close(timings, start, i, j):
+    if timings is None:
+        return
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    timings.append((i, j, start, e))
+
+
 def virtual_ring_backward(douts, qs, ks, vs, outs, lses, *, layout: str = "striped",
-                          softmax_scale: float, block_ops: BlockOps | None = None):
+                          softmax_scale: float, block_ops: BlockOps | None = None,
+                          timings: list | None = None, cast: bool = True):
     """Backward over all N stripes on one device; dK/dV accumulators stay with their
-    stripe (index ``held``), exactly what the travelling buffers compute."""
+    stripe (index ``held``), exactly what the travelling buffers compute.  ``cast=False``
+    returns the fp32 accumulators (timing runs)."""
     bops = block_ops or BlockOps()
     n = len(qs)
     c, hq, d = qs[0].shape
@@ -419,8 +679,12 @@ def virtual_ring_backward(douts, qs, ks, vs, outs, lses, *, layout: str = "strip
         for j in range(n):
             held = (j - i) % n
             kind = masks.block_mask(layout, j, held, n)
+            ev = _ev_pair(timings)
             bops.bwd_block(qs[j], ks[held], vs[held], douts[j], lses[j], dsums[j], dqs[j],
                            dks[held], dvs[held], softmax_scale, kind)
+            _ev_close(timings, ev, i, j)
+    if not cast:
+        return dqs, dks, dvs
     res = []
     for acc, like in ((dqs, qs), (dks, ks), (dvs, vs)):
         outl = []

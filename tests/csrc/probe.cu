@@ -2,8 +2,57 @@
 //   s = a b^T          (SS MMA, both operands K-major: the QK^T shape)
 //   o = bf16(s) v      (TS MMA, A from TMEM, B MN-major: the PV shape)
 //   y = b^T v          (SS MMA, A MN-major, B MN-major: the dS^T Q / dS K shapes)
+// Built into tests/csrc/libsa_probe.so (test infrastructure, not the product library).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <string>
+
 #include "common.cuh"
-#include "internal.h"
+
+namespace sa {
+namespace {
+thread_local std::string g_probe_err;
+
+int probe_check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_probe_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return -static_cast<int>(e);
+  }
+  return 0;
+}
+
+// 2-D bf16 [rows, cols] map, box (64 x box_rows), SW128.
+int make_tmap_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int32_t box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess) {
+      g_probe_err = "cuTensorMapEncodeTiled unavailable";
+      return 1;
+    }
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t sizes[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), sizes,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_probe_err = "cuTensorMapEncodeTiled(2d) failed";
+    return 1;
+  }
+  return 0;
+}
+}  // namespace
+}  // namespace sa
 
 namespace sa {
 namespace {
@@ -109,7 +158,7 @@ int launch_probe(const void* a, const void* b, const void* v, float* s, float* o
   const int smem = 6 * kPanel + 1024;
   cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   probe_kernel<<<1, 128, smem, st>>>(ta, tb, tv, s, o, y);
-  return check_launch("probe_kernel");
+  return probe_check_launch("probe_kernel");
 }
 
 }  // namespace sa
@@ -241,7 +290,24 @@ int launch_probe_pair(const void* a, const void* b, const void* v, float* s, flo
   const int smem = 4 * kPanel + 1024;
   cudaFuncSetAttribute(probe_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   probe_pair_kernel<<<2, 128, smem, st>>>(ta, tb, tv, s, o, s2);
-  return check_launch("probe_pair_kernel");
+  return probe_check_launch("probe_pair_kernel");
 }
 
 }  // namespace sa
+
+// ---------------------------------------------------------------------------------------
+extern "C" {
+const char* sa_probe_last_error(void) { return sa::g_probe_err.c_str(); }
+
+int sa_probe_umma(const void* a, const void* b, const void* v, float* s, float* o, float* y,
+                  void* stream) {
+  if (!a || !b || !v || !s || !o || !y) return 1;
+  return sa::launch_probe(a, b, v, s, o, y, static_cast<cudaStream_t>(stream));
+}
+
+int sa_probe_pair(const void* a, const void* b, const void* v, float* s, float* o, float* s2,
+                  void* stream) {
+  if (!a || !b || !v || !s || !o || !s2) return 1;
+  return sa::launch_probe_pair(a, b, v, s, o, s2, static_cast<cudaStream_t>(stream));
+}
+}  // extern "C"

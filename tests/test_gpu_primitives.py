@@ -18,7 +18,8 @@ def ops():
 def test_umma_probe_layouts(ops):
     g = torch.Generator(device="cuda").manual_seed(0)
     a, b, v = (torch.randn(128, 128, device="cuda", generator=g).bfloat16() for _ in range(3))
-    s, o, y = ops.probe_umma(a, b, v)
+    import probe_lib
+    s, o, y = probe_lib.probe_umma(a, b, v)
     torch.cuda.synchronize()
     s_ref = a.float() @ b.float().T
     o_ref = s.bfloat16().float() @ v.float()
@@ -34,7 +35,8 @@ def test_umma_pair_probe_layouts(ops):
     a = torch.randn(256, 128, device="cuda", generator=g).bfloat16()
     b = torch.randn(128, 128, device="cuda", generator=g).bfloat16()
     v = torch.randn(128, 128, device="cuda", generator=g).bfloat16()
-    s, o, s2 = ops.probe_pair(a, b, v)
+    import probe_lib
+    s, o, s2 = probe_lib.probe_pair(a, b, v)
     torch.cuda.synchronize()
     s_ref = a.float() @ b.float().T
     assert (s - s_ref).abs().max().item() < 1e-3
