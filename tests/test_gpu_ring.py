@@ -213,7 +213,8 @@ def test_ringsim_shaped_shim_matches_reference(name):
     n_dev, n_seq, heads, d, tile, _ = g["meta"].tolist()
     cfg = SimpleNamespace(algo=str(g["algo"]), n_devices=n_dev, n_seq=n_seq, d_head=d,
                           tile_q=tile, tile_k=tile, scale=True, precision="double")
-    out, _, stats = compat.simulate_gpu(cfg, (g["q"][:, 0], g["k"][:, 0], g["v"][:, 0]))
+    run = compat.simulate_gpu(cfg, (g["q"][:, 0], g["k"][:, 0], g["v"][:, 0]))
+    out, stats = run.output, run.stats
     check(out, g["o"][:, 0], "out")
     got = [[[r.round, r.block_index, r.tiles_total, r.tiles_skipped, r.tiles_partial,
              r.tiles_full, r.interactions_computed, r.interactions_required] for r in ws.rounds]
