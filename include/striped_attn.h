@@ -114,6 +114,21 @@ int sa_bwd_block_final(const void* q, const void* k, const void* v, const void* 
                        int64_t c, int32_t hq, int32_t hkv, int32_t d, float softmax_scale,
                        int32_t mask_kind, void* stream);
 
+/* All options of K5 in one entry point:
+ *   - dk_acc / dv_acc (fp32, reduce-added) OR dk_out / dv_out (bf16, written; whole key
+ *     range only) -- exactly one pair non-NULL;
+ *   - key rows [key_row_begin, key_row_end) as sa_bwd_block_range (key_row_end < 0 = c);
+ *   - dq_semaphore (nullable): DETERMINISTIC dQ.  int32 [hq, ceil(c/128)], zero-filled
+ *     once by the caller and left zero by every launch; the key tiles then add into each
+ *     query tile of dq_acc in ascending order, so reruns are bit-identical (the
+ *     reference requires reproducible runs: verify.py:216-227).  Slower: the
+ *     reduce-adds of one query tile serialise across CTAs. */
+int sa_bwd_block_ex(const void* q, const void* k, const void* v, const void* dout,
+                    const float* lse, const float* dsum, float* dq_acc, float* dk_acc,
+                    float* dv_acc, void* dk_out, void* dv_out, int64_t c, int32_t hq, int32_t hkv,
+                    int32_t d, float softmax_scale, int32_t mask_kind, int32_t key_row_begin,
+                    int32_t key_row_end, int32_t* dq_semaphore, void* stream);
+
 int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
 
 /* Strided host<->device row copy (cudaMemcpy2DAsync): `height` rows of `width` bytes,
@@ -127,6 +142,18 @@ int sa_memcpy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch
  * (ring.LocalComm, ipc.IpcComm) -- the reference's per-round message hand-off,
  * simulator.py:211-215 -- issued without NCCL kernels on the SMs. */
 int sa_memcpy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* CUDA IPC for the one-process-per-GPU copy-engine hop (ipc.IpcComm), handles exchanged
+ * once per buffer: 64-byte opaque handles.  sa_ipc_mem_handle returns the handle of the
+ * allocation containing `ptr` and ptr's byte offset in it. */
+int sa_ipc_mem_handle(const void* ptr, void* handle_out, int64_t* offset_out);
+int sa_ipc_mem_open(const void* handle, void** base_out);
+int sa_ipc_mem_close(void* base);
+int sa_ipc_event_create(void** event_out, void* handle_out);
+int sa_ipc_event_open(const void* handle, void** event_out);
+int sa_event_record(void* event, void* stream);
+int sa_stream_wait_event(void* stream, void* event);
+int sa_event_destroy(void* event);
 
 #ifdef __cplusplus
 }

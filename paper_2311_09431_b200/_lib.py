@@ -31,9 +31,19 @@ SIGNATURES = {
                                           _I32, _F32, _I32, _I32, _I32, _P]),
     "sa_bwd_block_final": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _I32,
                                           _I32, _F32, _I32, _P]),
+    "sa_bwd_block_ex": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32,
+                                       _I32, _I32, _F32, _I32, _I32, _I32, _P, _P]),
     "sa_cast_f32_bf16": (ctypes.c_int, [_P, _P, _I64, _P]),
     "sa_memcpy2d_async": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _P]),
     "sa_memcpy_async": (ctypes.c_int, [_P, _P, _I64, _P]),
+    "sa_ipc_mem_handle": (ctypes.c_int, [_P, _P, ctypes.POINTER(_I64)]),
+    "sa_ipc_mem_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "sa_ipc_mem_close": (ctypes.c_int, [_P]),
+    "sa_ipc_event_create": (ctypes.c_int, [ctypes.POINTER(_P), _P]),
+    "sa_ipc_event_open": (ctypes.c_int, [_P, ctypes.POINTER(_P)]),
+    "sa_event_record": (ctypes.c_int, [_P, _P]),
+    "sa_stream_wait_event": (ctypes.c_int, [_P, _P]),
+    "sa_event_destroy": (ctypes.c_int, [_P]),
 }
 
 

@@ -61,40 +61,45 @@ def striped_attn_forward(q, k, v, *, group=None, layout: str = "striped", softma
 
 
 def striped_attn_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped",
-                          softmax_scale=None):
-    """Backward -> (dq, dk, dv), bf16, same layout as the inputs."""
+                          softmax_scale=None, deterministic: bool = False):
+    """Backward -> (dq, dk, dv), bf16, same layout as the inputs.  ``deterministic``:
+    bit-identical reruns (ordered dQ reduction; slower)."""
     _check(q, k, v, layout)
     scale = _scale(q, softmax_scale)
     if q.dim() == 4:
         res = [striped_attn_backward(dout[b], q[b], k[b], v[b], out[b], lse[b], group=group,
-                                     layout=layout, softmax_scale=scale)
+                                     layout=layout, softmax_scale=scale,
+                                     deterministic=deterministic)
                for b in range(q.shape[0])]
         return tuple(torch.stack([r[i] for r in res]) for i in range(3))
     return ring.ring_backward(dout.contiguous(), q.contiguous(), k.contiguous(), v.contiguous(),
                               out.contiguous(), lse.contiguous(), group=group, layout=layout,
-                              softmax_scale=scale)
+                              softmax_scale=scale, deterministic=deterministic)
 
 
 class StripedAttnFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, group, layout, softmax_scale):
+    def forward(ctx, q, k, v, group, layout, softmax_scale, deterministic=False):
         out, lse = striped_attn_forward(q, k, v, group=group, layout=layout,
                                         softmax_scale=softmax_scale)
         ctx.save_for_backward(q, k, v, out, lse)
         ctx.group, ctx.layout, ctx.softmax_scale = group, layout, softmax_scale
+        ctx.deterministic = deterministic
         return out
 
     @staticmethod
     def backward(ctx, dout):
         q, k, v, out, lse = ctx.saved_tensors
         dq, dk, dv = striped_attn_backward(dout.contiguous(), q, k, v, out, lse, group=ctx.group,
-                                           layout=ctx.layout, softmax_scale=ctx.softmax_scale)
-        return dq, dk, dv, None, None, None
+                                           layout=ctx.layout, softmax_scale=ctx.softmax_scale,
+                                           deterministic=ctx.deterministic)
+        return dq, dk, dv, None, None, None, None
 
 
-def striped_attention(q, k, v, group=None, layout: str = "striped", softmax_scale=None):
+def striped_attention(q, k, v, group=None, layout: str = "striped", softmax_scale=None,
+                      deterministic: bool = False):
     """Autograd entry point: returns O for this rank's stripe."""
-    return StripedAttnFunction.apply(q, k, v, group, layout, softmax_scale)
+    return StripedAttnFunction.apply(q, k, v, group, layout, softmax_scale, deterministic)
 
 
 def ring_attention(q, k, v, group=None, softmax_scale=None):

@@ -203,6 +203,43 @@ int sa_bwd_block_final(const void* q, const void* k, const void* v, const void* 
                     softmax_scale, mask_kind, st, dk, dv);
 }
 
+int sa_bwd_block_ex(const void* q, const void* k, const void* v, const void* dout,
+                    const float* lse, const float* dsum, float* dq_acc, float* dk_acc,
+                    float* dv_acc, void* dk_out, void* dv_out, int64_t c, int32_t hq, int32_t hkv,
+                    int32_t d, float softmax_scale, int32_t mask_kind, int32_t key_row_begin,
+                    int32_t key_row_end, int32_t* dq_semaphore, void* stream) {
+  if (int r = check_heads(c, hq, hkv, d)) return r;
+  const bool final_out = dk_out || dv_out;
+  if (final_out && (!dk_out || !dv_out)) return fail_arg("dk_out and dv_out go together");
+  if (!final_out && (!dk_acc || !dv_acc)) return fail_arg("need dk_acc/dv_acc or dk_out/dv_out");
+  if (!q || !k || !v || !dout || !lse || !dsum || !dq_acc) return fail_arg("null pointer");
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(dout) || !aligned16(dq_acc) ||
+      (dk_acc && !aligned16(dk_acc)) || (dv_acc && !aligned16(dv_acc)) ||
+      (dk_out && !aligned16(dk_out)) || (dv_out && !aligned16(dv_out)))
+    return fail_arg("q/k/v/dout, dq_acc and the dK/dV buffers must be 16B aligned");
+  if (mask_kind < 0 || mask_kind > 3) return fail_arg("bad mask kind");
+  if (!(softmax_scale > 0.f)) return fail_arg("softmax_scale must be > 0");
+  if (key_row_end < 0) key_row_end = static_cast<int32_t>(c);
+  if (key_row_begin < 0 || key_row_end > c || key_row_begin > key_row_end ||
+      key_row_begin % 128 || (key_row_end % 128 && key_row_end != c))
+    return fail_arg("key rows must be a 128-aligned sub-range of [0, c)");
+  if (final_out && (key_row_begin != 0 || key_row_end != c))
+    return fail_arg("bf16 dK/dV outputs need the whole key range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (mask_kind == SA_MASK_FULLY_MASKED || key_row_begin == key_row_end) {
+    if (final_out) {
+      const size_t bytes = static_cast<size_t>(c) * hkv * d * 2;
+      if (cudaMemsetAsync(dk_out, 0, bytes, st) != cudaSuccess ||
+          cudaMemsetAsync(dv_out, 0, bytes, st) != cudaSuccess)
+        return check_launch("memset dk/dv");
+    }
+    return 0;
+  }
+  return launch_bwd(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, c, hq, hkv, d,
+                    softmax_scale, mask_kind, st, dk_out, dv_out, key_row_begin / 128,
+                    (key_row_end + 127) / 128, dq_semaphore);
+}
+
 int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream) {
   if (!src || !dst || n < 0) return fail_arg("bad cast arguments");
   if (n == 0) return 0;

@@ -56,6 +56,9 @@ struct BwdParams {
   // bf16 straight from TMEM instead of reduce-added into fp32 accumulators
   __nv_bfloat16* dk_out;
   __nv_bfloat16* dv_out;
+  // deterministic dQ (nullable): int32 [hq, n_t] ordering the reduce-adds into each query
+  // tile by ascending key tile; zero at launch, left zero by the launch
+  int* dq_sem;
   int c, hq, hkv, n_t;
   int j_begin, n_j;  // key tiles [j_begin, j_begin + n_j) of the block (a part of it)
   float scale, scale_log2;
@@ -488,6 +491,17 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       mbar_arrive(&bar[B_DQ_FREE]);
       if (leader) SA_TR(18);
       if (SA_PERF_TRACE && (p.debug & 1)) continue;
+      int* sem = p.dq_sem ? p.dq_sem + (int64_t)h * p.n_t + i : nullptr;
+      if (sem && leader) {
+        // deterministic dQ: the key tiles add into query tile i in ascending j order.  The
+        // CTAs of lower j have lower blockIdx (scheduled earlier), so the wait cannot
+        // deadlock; the semaphore counts this launch's contributions to tile i.
+        const int want = j - p.j_begin;
+        uint32_t spins = 0;
+        while (ld_acquire_gpu(sem) != want)
+          if (++spins > (1u << 30)) __trap();
+        fence_proxy_async_global();  // the previous adder's TMA writes before ours
+      }
 #pragma unroll
       for (int ch = 0; ch < kChunks; ch++) {
         const uint32_t buf = sbase + L::kStg + (ch & 1) * kPanelBytes;
@@ -507,6 +521,13 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
             tma_reduce_add_3d(&p.tdq, smem + L::kStg + (ch & 1) * kPanelBytes, 32 * ch, h, 128 * i);
           bulk_commit();
         }
+      }
+      if (sem && leader) {
+        bulk_wait<0>();              // our adds are complete in global memory
+        fence_proxy_async_global();
+        // the last contributor of this launch leaves the semaphore zeroed for the next one
+        const int j_last = causal ? min(i, p.j_begin + p.n_j - 1) : p.j_begin + p.n_j - 1;
+        st_release_gpu(sem, j == j_last ? 0 : j - p.j_begin + 1);
       }
       if (leader) SA_TR(19);
     }
@@ -563,8 +584,10 @@ int launch_bwd_d(BwdParams& prm, cudaStream_t st) {
 int launch_bwd(const void* q, const void* k, const void* v, const void* dout, const float* lse,
                const float* dsum, float* dq, float* dk, float* dv, int64_t c, int32_t hq,
                int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st,
-               void* dk_out, void* dv_out, int32_t kv_tile_begin, int32_t kv_tile_end) {
+               void* dk_out, void* dv_out, int32_t kv_tile_begin, int32_t kv_tile_end,
+               int32_t* dq_sem) {
   BwdParams prm;
+  prm.dq_sem = dq_sem;
   prm.dk_out = static_cast<__nv_bfloat16*>(dk_out);
   prm.dv_out = static_cast<__nv_bfloat16*>(dv_out);
   if (int r = make_tmap_rows(&prm.tq, q, c, hq, d, 128)) return r;

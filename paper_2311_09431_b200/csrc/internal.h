@@ -58,7 +58,7 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
                const float* dsum, float* dq, float* dk, float* dv, int64_t c, int32_t hq,
                int32_t hkv, int32_t d, float scale, int32_t kind, cudaStream_t st,
                void* dk_out = nullptr, void* dv_out = nullptr, int32_t kv_tile_begin = 0,
-               int32_t kv_tile_end = -1);
+               int32_t kv_tile_end = -1, int32_t* dq_sem = nullptr);
 int launch_cast(const float* src, void* dst, int64_t n, cudaStream_t st);
 int launch_fill_state(float* o_acc, float* lse, int64_t c, int32_t hq, int32_t d, cudaStream_t st);
 

@@ -87,10 +87,21 @@ def bwd_preprocess(out, dout, dsum, dq_acc):
                    "sa_bwd_preprocess")
 
 
+def _sem_ptr(dq_sem, hq, c):
+    if dq_sem is None:
+        return None
+    if not (isinstance(dq_sem, torch.Tensor) and dq_sem.is_cuda and dq_sem.dtype == torch.int32):
+        raise ValueError("dq_sem must be a CUDA int32 tensor")
+    if dq_sem.numel() < hq * ((c + 127) // 128):
+        raise ValueError(f"dq_sem needs hq * ceil(c / 128) = {hq * ((c + 127) // 128)} entries")
+    return dq_sem.data_ptr()
+
+
 def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: float,
-              mask_kind: int, key_rows=None):
+              mask_kind: int, key_rows=None, dq_sem=None):
     """K5: one ring step of the backward (accumulates into dq_acc / dk_acc / dv_acc);
-    ``key_rows=(r0, r1)`` restricts it to those held-stripe keys (sa_bwd_block_range)."""
+    ``key_rows=(r0, r1)`` restricts it to those held-stripe keys (sa_bwd_block_range);
+    ``dq_sem`` (zeroed int32 [hq * ceil(c/128)]) makes the dQ reduction deterministic."""
     for n, t in (("q", q), ("k", k), ("v", v), ("dout", dout)):
         _need_cuda(n, t, torch.bfloat16)
     for n, t in (("lse", lse), ("dsum", dsum), ("dq_acc", dq_acc), ("dk_acc", dk_acc),
@@ -99,7 +110,14 @@ def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: f
     c, hq, d = q.shape
     hkv = k.shape[1]
     with _on(q):
-        if key_rows is None:
+        if dq_sem is not None:
+            r0, r1 = key_rows if key_rows is not None else (0, c)
+            _lib.check(_lib.lib().sa_bwd_block_ex(
+                q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                dsum.data_ptr(), dq_acc.data_ptr(), dk_acc.data_ptr(), dv_acc.data_ptr(), None,
+                None, c, hq, hkv, d, float(softmax_scale), int(mask_kind), int(r0), int(r1),
+                _sem_ptr(dq_sem, hq, c), _stream(q)), "sa_bwd_block_ex")
+        elif key_rows is None:
             _lib.check(_lib.lib().sa_bwd_block(
                 q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                 dsum.data_ptr(), dq_acc.data_ptr(), dk_acc.data_ptr(), dv_acc.data_ptr(), c, hq,
@@ -113,9 +131,9 @@ def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: f
 
 
 def bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, softmax_scale: float,
-                    mask_kind: int):
+                    mask_kind: int, dq_sem=None):
     """K5 for a block that is the only contribution to dK / dV: dk / dv (bf16 [c, Hkv, D])
-    are written, not accumulated (sa_bwd_block_final)."""
+    are written, not accumulated (sa_bwd_block_final; sa_bwd_block_ex with ``dq_sem``)."""
     for n, t in (("q", q), ("k", k), ("v", v), ("dout", dout), ("dk", dk), ("dv", dv)):
         _need_cuda(n, t, torch.bfloat16)
     for n, t in (("lse", lse), ("dsum", dsum), ("dq_acc", dq_acc)):
@@ -123,6 +141,13 @@ def bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, softmax_scale: flo
     c, hq, d = q.shape
     hkv = k.shape[1]
     with _on(q):
+        if dq_sem is not None:
+            _lib.check(_lib.lib().sa_bwd_block_ex(
+                q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                dsum.data_ptr(), dq_acc.data_ptr(), None, None, dk.data_ptr(), dv.data_ptr(), c,
+                hq, hkv, d, float(softmax_scale), int(mask_kind), 0, int(c),
+                _sem_ptr(dq_sem, hq, c), _stream(q)), "sa_bwd_block_ex")
+            return
         _lib.check(_lib.lib().sa_bwd_block_final(
             q.data_ptr(), k.data_ptr(), v.data_ptr(), dout.data_ptr(), lse.data_ptr(),
             dsum.data_ptr(), dq_acc.data_ptr(), dk.data_ptr(), dv.data_ptr(), c, hq, hkv, d,

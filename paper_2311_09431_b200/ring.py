@@ -58,13 +58,15 @@ class BlockOps:
         self._ops.bwd_preprocess(out, dout, dsum, dq_acc)
 
     def bwd_block(self, q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind,
-                  key_rows=None):
+                  key_rows=None, dq_sem=None):
         self._ops.bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, scale, kind,
-                            key_rows)
+                            key_rows, dq_sem)
 
-    def bwd_block_final(self, q, k, v, dout, lse, dsum, dq_acc, dk, dv, scale, kind):
+    def bwd_block_final(self, q, k, v, dout, lse, dsum, dq_acc, dk, dv, scale, kind,
+                        dq_sem=None):
         """Single-step backward: bf16 dK / dV written directly (no accumulators / casts)."""
-        self._ops.bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, scale, kind)
+        self._ops.bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, scale, kind,
+                                  dq_sem)
 
     def cast(self, src, dst):
         self._ops.cast_f32_bf16(src, dst)
@@ -509,8 +511,12 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
 def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped",
                   softmax_scale: float, block_ops: BlockOps | None = None,
                   stats: RingStats | None = None, workspace: Workspace | None = None,
-                  comm: Comm | None = None):
+                  comm: Comm | None = None, deterministic: bool = False):
     """Backward for this rank's stripe -> (dq, dk, dv) bf16 in local order.
+
+    ``deterministic``: the dQ reduce-adds of every launch happen in a fixed order (a
+    zeroed int32 semaphore per query tile, see sa_bwd_block_ex), so reruns are
+    bit-identical (verify.py:216-227); dK / dV are deterministic either way.
 
     Per round the held block runs in key parts (``kv_parts``); each part's fp32 dK/dV
     rows hop to the next rank on the dK/dV stream as soon as the part retires, and the
@@ -528,6 +534,9 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
     dsum = _alloc(ws, "dsum", (hq, c), torch.float32, dev)
     dq_acc = _alloc(ws, "dq_acc", (c, hq, d), torch.float32, dev)
     bops.bwd_preprocess(out, dout, dsum, dq_acc)
+    det = {}
+    if deterministic:
+        det["dq_sem"] = _alloc(ws, "dq_sem", (hq * (-(-c // 128)),), torch.int32, dev, zero=True)
     timer = _StepTimer(q, stats is not None)
     if world == 1 and hasattr(bops, "bwd_block_final"):
         # one step: dK / dV come out of the kernel as bf16 (no fp32 accumulators / casts)
@@ -535,7 +544,8 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
         dk = _alloc(ws, "dk", k.shape, k.dtype, dev)
         dv = _alloc(ws, "dv", v.shape, v.dtype, dev)
         timer.start()
-        bops.bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, softmax_scale, kind)
+        bops.bwd_block_final(q, k, v, dout, lse, dsum, dq_acc, dk, dv, softmax_scale, kind,
+                             **det)
         timer.stop()
         if stats is not None:
             stats.rounds.append(StepRecord(0, 0, int(kind)))
@@ -548,7 +558,8 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
     if world == 1:
         kind = masks.block_mask(layout, 0, 0, 1)
         timer.start()
-        bops.bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale, kind)
+        bops.bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale, kind,
+                       **det)
         timer.stop()
         if stats is not None:
             stats.rounds.append(StepRecord(0, 0, int(kind)))
@@ -574,7 +585,7 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
             for pi, (r0, r1) in enumerate(parts):
                 st.wait(st.compute, arrived[pi])  # this part's accumulator rows are here
                 bops.bwd_block(q, cur[0], cur[1], dout, lse, dsum, dq_acc, dcur[0], dcur[1],
-                               softmax_scale, kind, key_rows=(r0, r1))
+                               softmax_scale, kind, key_rows=(r0, r1), **det)
                 st.wait(st.dkv, st.event(st.compute))
                 with st.on(st.dkv):
                     h0 = hops.start(st.dkv)
