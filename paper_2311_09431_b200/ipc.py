@@ -38,8 +38,18 @@ def _handle_bytes(buf) -> bytes:
     return bytes(bytearray(buf))
 
 
+class _DevPtr:
+    """A raw device pointer as a __cuda_array_interface__ object (zero-copy torch view)."""
+
+    def __init__(self, ptr: int, shape, dtype: torch.dtype):
+        typestr = {torch.float32: "<f4", torch.bfloat16: "<V2", torch.int32: "<i4"}[dtype]
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2, "strides": None}
+
+
 class IpcComm(Comm):
     name = "ipc"
+    peer_memory = True
 
     def __init__(self, group=None, store=None, timeout: float = STALL_TIMEOUT_S):
         self.group = group
@@ -57,7 +67,9 @@ class IpcComm(Comm):
         self._lib = _lib.lib()
         self._free_ev, free_h = self._create_event()
         self._done_ev, done_h = self._create_event()
-        self.store.set(f"{self.prefix}ev/{self.rank}", pickle.dumps((free_h, done_h)))
+        self._sync_ev, sync_h = self._create_event()
+        self.store.set(f"{self.prefix}ev/{self.rank}", pickle.dumps((free_h, done_h, sync_h)))
+        self._n = 0  # collective sequence number (peer_views / sync_all)
         self._peer_ev = {}   # (rank, which) -> opened event
         self._opened = {}    # handle bytes -> opened base pointer
         self._mine = {}      # local base pointer -> (handle bytes)
@@ -138,6 +150,51 @@ class IpcComm(Comm):
         self._get(f"{self.prefix}done/{self.prev_rank}/{s}")
         self._check(self._lib.sa_stream_wait_event(stream, self._peer_event(self.prev_rank, 1)),
                     "sa_stream_wait_event")
+
+    # ------------------------------------------------------------------ collectives
+    def _all_gather(self, tag, value: bytes) -> list:
+        n = self._n
+        self._n += 1
+        self.store.set(f"{self.prefix}{tag}/{n}/{self.rank}", value)
+        out = [self.store.get(f"{self.prefix}{tag}/{n}/{j}") for j in range(self.world)]
+        # nobody deletes a key before every rank has read it: acknowledge, then clean up
+        self.store.set(f"{self.prefix}{tag}_ack/{n}/{self.rank}", b"1")
+        for j in range(self.world):
+            self.store.get(f"{self.prefix}{tag}_ack/{n}/{j}")
+        return out
+
+    def peer_views(self, t):
+        if t.dtype != torch.float32 or not t.is_contiguous():
+            raise ValueError("peer_views: contiguous fp32 buffers only")
+        mine = pickle.dumps(self._describe(t))
+        views = []
+        for j, blob in enumerate(self._all_gather("views", mine)):
+            if j == self.rank:
+                views.append(t)
+                continue
+            handle, off, nbytes = pickle.loads(blob)
+            if nbytes != t.numel() * t.element_size():
+                raise RuntimeError("peer buffers differ in size")
+            ptr = self._open(handle) + off
+            views.append(torch.as_tensor(_DevPtr(ptr, t.shape, t.dtype), device=t.device))
+        return views
+
+    def sync_all(self, ref):
+        stream = torch.cuda.current_stream(ref.device).cuda_stream
+        self._check(self._lib.sa_event_record(self._sync_ev, stream), "sa_event_record")
+        n = self._n
+        self._n += 1
+        key = lambda j: f"{self.prefix}sync/{n}/{j}"
+        self.store.set(key(self.rank), b"1")
+        for j in range(self.world):
+            if j != self.rank:
+                self.store.get(key(j))
+                self._check(self._lib.sa_stream_wait_event(stream, self._peer_event(j, 2)),
+                            "sa_stream_wait_event")
+        # the next record of any rank's sync event must follow every rank's wait on it
+        self.store.set(f"{self.prefix}sync_ack/{n}/{self.rank}", b"1")
+        for j in range(self.world):
+            self.store.get(f"{self.prefix}sync_ack/{n}/{j}")
 
     def close(self):
         for base in self._opened.values():

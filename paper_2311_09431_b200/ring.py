@@ -110,8 +110,20 @@ class Comm:
     rank: int = 0
     world: int = 1
     name: str = "comm"
+    # backends whose ranks can address each other's device memory (LocalComm threads,
+    # IpcComm processes) also provide peer_views / sync_all, used by the fused backward
+    peer_memory: bool = False
 
     def exchange(self, send, recv):  # pragma: no cover - interface
+        raise NotImplementedError
+
+    def peer_views(self, t: torch.Tensor) -> list:  # pragma: no cover - interface
+        """Every rank's tensor ``t`` (same shape / dtype on all ranks), addressable here."""
+        raise NotImplementedError
+
+    def sync_all(self, ref: torch.Tensor) -> None:  # pragma: no cover - interface
+        """Stream-level barrier: work every rank enqueued before the call precedes work
+        any rank enqueues after it (on the current streams)."""
         raise NotImplementedError
 
 
@@ -224,6 +236,7 @@ class LocalComm(Comm):
     (the enqueued work stays acyclic)."""
 
     name = "local"
+    peer_memory = True
 
     def __init__(self, ring: LocalRing, rank: int):
         self.ring = ring
@@ -231,6 +244,23 @@ class LocalComm(Comm):
         self.world = ring.world
         self.next = (rank + 1) % ring.world
         self.prev = (rank - 1) % ring.world
+        self._n = 0  # collective sequence number (every rank calls in the same order)
+
+    def _key(self, what):
+        self._n += 1
+        return (what, self._n)
+
+    def peer_views(self, t):
+        return self.ring.all_gather(self.rank, self._key("views"), t)
+
+    def sync_all(self, ref):
+        ev = _record(ref) if ref.is_cuda else None
+        evs = self.ring.all_gather(self.rank, self._key("sync"), ev)
+        if ref.is_cuda:
+            cur = torch.cuda.current_stream(ref.device)
+            for j, e in enumerate(evs):
+                if j != self.rank:
+                    cur.wait_event(e)
 
     def exchange(self, send, recv):
         r = self.ring
@@ -511,8 +541,12 @@ def ring_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale:
 def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped",
                   softmax_scale: float, block_ops: BlockOps | None = None,
                   stats: RingStats | None = None, workspace: Workspace | None = None,
-                  comm: Comm | None = None, deterministic: bool = False):
+                  comm: Comm | None = None, deterministic: bool = False,
+                  fused_dkv: bool = False):
     """Backward for this rank's stripe -> (dq, dk, dv) bf16 in local order.
+
+    ``fused_dkv`` (peer-memory comms only): no dK/dV hops -- each round's kernel adds
+    into the held stripe's home accumulator on its owner rank directly (see below).
 
     ``deterministic``: the dQ reduce-adds of every launch happen in a fixed order (a
     zeroed int32 semaphore per query tile, see sa_bwd_block_ex), so reruns are
@@ -563,6 +597,49 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
         timer.stop()
         if stats is not None:
             stats.rounds.append(StepRecord(0, 0, int(kind)))
+    elif fused_dkv:
+        # SURVEY 8(f)3, fused rotation: no dK/dV hop at all.  Every stripe's fp32 dK/dV
+        # accumulator stays on its home rank; the block kernel of whichever rank holds the
+        # stripe in a round reduce-adds its contribution straight into the home buffer
+        # through peer memory (NVLink) from its epilogue, tile by tile as CTAs retire.
+        if deterministic:
+            raise ValueError("fused_dkv adds into the home buffers in arrival order; "
+                             "use the travelling accumulators for deterministic=True")
+        if not getattr(comm, "peer_memory", False):
+            raise ValueError(f"fused_dkv needs a peer-memory comm (LocalComm / IpcComm), "
+                             f"got {getattr(comm, 'name', comm)!r}")
+        st = _Streams(q)
+        hops = _HopTimer(st, stats)
+        homes_k = comm.peer_views(dk_acc)
+        homes_v = comm.peer_views(dv_acc)
+        comm.sync_all(q)  # every home buffer is zeroed before anyone adds into it
+        kv_bufs = [(_alloc(ws, f"bkbuf{b}", k.shape, k.dtype, dev),
+                    _alloc(ws, f"bvbuf{b}", v.shape, v.dtype, dev)) for b in range(2)]
+        cur = (k, v)
+        for i in range(world):
+            held = (rank - i) % world
+            nxt = kv_bufs[i % 2]
+            kv_ready = None
+            if i < world - 1:
+                st.wait(st.kv, st.event(st.compute))
+                with st.on(st.kv):
+                    h0 = hops.start(st.kv)
+                    comm.exchange(list(cur), list(nxt))
+                    hops.stop(st.kv, h0, i, "kv", cur)
+                kv_ready = st.event(st.kv)
+            kind = masks.block_mask(layout, rank, held, world)
+            timer.start()
+            bops.bwd_block(q, cur[0], cur[1], dout, lse, dsum, dq_acc, homes_k[held],
+                           homes_v[held], softmax_scale, kind)
+            timer.stop()
+            if stats is not None:
+                stats.rounds.append(StepRecord(i, held, int(kind)))
+            if i < world - 1:
+                st.wait(st.compute, kv_ready)
+                cur = nxt
+        comm.sync_all(q)  # every rank's contributions to my stripe are in
+        if stats is not None:
+            hops.fill()
     else:
         st = _Streams(q)
         hops = _HopTimer(st, stats)

@@ -5,6 +5,8 @@ with this injected per-step compute so rotation, double buffering, LSE merging a
 travelling dK/dV accumulators can be checked over real process groups without a GPU.
 """
 
+import threading
+
 import numpy as np
 import torch
 
@@ -16,6 +18,10 @@ def _np(t):
 
 
 class OracleBlockOps:
+    # the fused backward adds into peer threads' home buffers: serialise the in-place adds
+    # (the GPU path uses hardware reduce-adds)
+    _add_lock = threading.Lock()
+
     def __init__(self):
         self.calls = []
 
@@ -52,8 +58,9 @@ class OracleBlockOps:
         dq, dk, dv = R.block_backward(_np(q), _np(k), _np(v), _np(dout), _np(lse), _np(dsum),
                                       int(kind), scale, key_rows=key_rows)
         dq_acc += torch.tensor(dq, dtype=dq_acc.dtype)
-        dk_acc += torch.tensor(dk, dtype=dk_acc.dtype)
-        dv_acc += torch.tensor(dv, dtype=dv_acc.dtype)
+        with self._add_lock:
+            dk_acc += torch.tensor(dk, dtype=dk_acc.dtype)
+            dv_acc += torch.tensor(dv, dtype=dv_acc.dtype)
 
     def cast(self, src, dst):
         dst.copy_(src.to(dst.dtype))

@@ -50,8 +50,10 @@ def _check_np(got, want, name):
 
 
 # ------------------------------------------------------------------ configs[0], N = 4 ring
-@pytest.mark.parametrize("layout", ["striped", "ring"])
-def test_config0_ring_fwd_bwd_threads_on_one_gpu(layout):
+@pytest.mark.parametrize("layout,fused", [("striped", False), ("ring", False), ("striped", True)])
+def test_config0_ring_fwd_bwd_threads_on_one_gpu(layout, fused):
+    """fused=True: the fused rotation (no dK/dV hops; the kernels reduce-add into the
+    held stripe's home accumulator on its owner rank through peer memory)."""
     from paper_2311_09431_b200 import ring
     n_dev, n, h, d = 4, 8192, 8, 64
     scale = 1.0 / math.sqrt(d)
@@ -67,7 +69,8 @@ def test_config0_ring_fwd_bwd_threads_on_one_gpu(layout):
         out, lse = ring.ring_forward(t(q), t(k), t(v), layout=layout, softmax_scale=scale,
                                      comm=comm, stats=st)
         dq, dk, dv = ring.ring_backward(t(do), t(q), t(k), t(v), out, lse, layout=layout,
-                                        softmax_scale=scale, comm=comm, stats=st)
+                                        softmax_scale=scale, comm=comm, stats=st,
+                                        fused_dkv=fused)
         torch.cuda.current_stream().synchronize()
         return (rows, [r.block_index for r in st.rounds[:n_dev]],
                 *(x.float().cpu().numpy() for x in (out, lse, dq, dk, dv)))

@@ -29,7 +29,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, layout, n, hq, hkv, d, out_q):
+def _worker(rank, world, port, layout, n, hq, hkv, d, out_q, fused=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -55,7 +55,8 @@ def _worker(rank, world, port, layout, n, hq, hkv, d, out_q):
             out, lse = ring.ring_forward(t(q), t(k), t(v), layout=layout, softmax_scale=scale,
                                          comm=comm, stats=st)
             dq, dk, dv = ring.ring_backward(t(do), t(q), t(k), t(v), out, lse, layout=layout,
-                                            softmax_scale=scale, comm=comm, stats=st)
+                                            softmax_scale=scale, comm=comm, stats=st,
+                                            fused_dkv=fused)
             torch.cuda.current_stream().synchronize()
         res = [x.float().cpu().numpy() for x in (out, lse, dq, dk, dv)]
         hops = [(h.what, h.nbytes) for h in st.hops]
@@ -66,14 +67,18 @@ def _worker(rank, world, port, layout, n, hq, hkv, d, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("layout", ["striped", "ring"])
-def test_ipc_ring_processes_on_one_gpu(world, layout):
+@pytest.mark.parametrize("world,layout,fused", [(2, "striped", False), (4, "striped", False),
+                                                (2, "ring", False), (4, "ring", False),
+                                                (4, "striped", True)])
+def test_ipc_ring_processes_on_one_gpu(world, layout, fused):
+    """fused=True: no dK/dV hops; each process's kernels reduce-add into the other
+    processes' IPC-mapped home accumulators (the fused rotation of SURVEY 8(f)3)."""
     n, hq, hkv, d = 2048, 4, 2, 128
     ctx = mp.get_context("spawn")
     out_q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, n, hq, hkv, d, out_q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, layout, n, hq, hkv, d, out_q,
+                                               fused))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -97,4 +102,4 @@ def test_ipc_ring_processes_on_one_gpu(world, layout):
         kv = [b for w, b in hops if w == "kv"]
         assert len(kv) == 2 * (world - 1) and all(b == 2 * c * hkv * d * 2 for b in kv)
         dkv = [b for w, b in hops if w == "dkv"]
-        assert sum(dkv) == world * 2 * c * hkv * d * 4
+        assert sum(dkv) == (0 if fused else world * 2 * c * hkv * d * 4)

@@ -14,7 +14,7 @@ from cpu_blockops import OracleBlockOps
 from oracle import ringref as R
 
 
-def _run(world, c_rank, layout, hkv=2):
+def _run(world, c_rank, layout, hkv=2, fused=False):
     from paper_2311_09431_b200 import ring
     n, hq, d = c_rank * world, 4, 8
     rng = np.random.default_rng(11)
@@ -30,7 +30,8 @@ def _run(world, c_rank, layout, hkv=2):
         out, lse = ring.ring_forward(t(q), t(k), t(v), layout=layout, softmax_scale=0.3,
                                      block_ops=ops, stats=st, comm=comm)
         dq, dk, dv = ring.ring_backward(t(do), t(q), t(k), t(v), out, lse, layout=layout,
-                                        softmax_scale=0.3, block_ops=ops, comm=comm)
+                                        softmax_scale=0.3, block_ops=ops, comm=comm,
+                                        fused_dkv=fused)
         return rows, st, out, lse, dq, dk, dv
 
     res = ring.run_local_ring(world, rank_fn)
@@ -48,6 +49,26 @@ def _run(world, c_rank, layout, hkv=2):
 @pytest.mark.parametrize("layout", ["striped", "ring"])
 def test_local_ring_threads_match_oracle(world, c_rank, layout):
     _run(world, c_rank, layout)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("layout", ["striped", "ring"])
+def test_local_ring_fused_dkv_matches_oracle(world, layout):
+    """no dK/dV hops -- each round adds into the held stripe's home buffer
+    on its owner (peer memory), then a stream-level barrier before the casts."""
+    _run(world, 16, layout, fused=True)
+
+
+def test_fused_dkv_needs_peer_memory():
+    from paper_2311_09431_b200 import ring
+
+    class NoPeer(ring.Comm):
+        rank, world = 0, 2
+
+    q = torch.zeros(4, 1, 8)
+    with pytest.raises(ValueError, match="peer-memory"):
+        ring.ring_backward(q, q, q, q, q, torch.zeros(1, 4), softmax_scale=1.0,
+                           block_ops=OracleBlockOps(), comm=NoPeer(), fused_dkv=True)
 
 
 def test_local_ring_failure_aborts_instead_of_hanging():
