@@ -118,7 +118,7 @@ int sa_bwd_block_final(const void* q, const void* k, const void* v, const void* 
  *   - dk_acc / dv_acc (fp32, reduce-added) OR dk_out / dv_out (bf16, written; whole key
  *     range only) -- exactly one pair non-NULL;
  *   - key rows [key_row_begin, key_row_end) as sa_bwd_block_range (key_row_end < 0 = c);
- *   - dq_semaphore (nullable): DETERMINISTIC dQ.  int32 [hq, ceil(c/128)], zero-filled
+ *   - dq_semaphore (nullable): DETERMINISTIC dQ.  int32 [hq, ceil(c/64)], zero-filled
  *     once by the caller and left zero by every launch; the key tiles then add into each
  *     query tile of dq_acc in ascending order, so reruns are bit-identical (the
  *     reference requires reproducible runs: verify.py:216-227).  Slower: the

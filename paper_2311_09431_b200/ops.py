@@ -92,8 +92,8 @@ def _sem_ptr(dq_sem, hq, c):
         return None
     if not (isinstance(dq_sem, torch.Tensor) and dq_sem.is_cuda and dq_sem.dtype == torch.int32):
         raise ValueError("dq_sem must be a CUDA int32 tensor")
-    if dq_sem.numel() < hq * ((c + 127) // 128):
-        raise ValueError(f"dq_sem needs hq * ceil(c / 128) = {hq * ((c + 127) // 128)} entries")
+    if dq_sem.numel() < hq * ((c + 63) // 64):
+        raise ValueError(f"dq_sem needs hq * ceil(c / 64) = {hq * ((c + 63) // 64)} entries")
     return dq_sem.data_ptr()
 
 
@@ -101,7 +101,7 @@ def bwd_block(q, k, v, dout, lse, dsum, dq_acc, dk_acc, dv_acc, softmax_scale: f
               mask_kind: int, key_rows=None, dq_sem=None):
     """K5: one ring step of the backward (accumulates into dq_acc / dk_acc / dv_acc);
     ``key_rows=(r0, r1)`` restricts it to those held-stripe keys (sa_bwd_block_range);
-    ``dq_sem`` (zeroed int32 [hq * ceil(c/128)]) makes the dQ reduction deterministic."""
+    ``dq_sem`` (zeroed int32 [hq * ceil(c/64)]) makes the dQ reduction deterministic."""
     for n, t in (("q", q), ("k", k), ("v", v), ("dout", dout)):
         _need_cuda(n, t, torch.bfloat16)
     for n, t in (("lse", lse), ("dsum", dsum), ("dq_acc", dq_acc), ("dk_acc", dk_acc),

@@ -570,7 +570,7 @@ def ring_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped
     bops.bwd_preprocess(out, dout, dsum, dq_acc)
     det = {}
     if deterministic:
-        det["dq_sem"] = _alloc(ws, "dq_sem", (hq * (-(-c // 128)),), torch.int32, dev, zero=True)
+        det["dq_sem"] = _alloc(ws, "dq_sem", (hq * (-(-c // 64)),), torch.int32, dev, zero=True)
     timer = _StepTimer(q, stats is not None)
     if world == 1 and hasattr(bops, "bwd_block_final"):
         # one step: dK / dV come out of the kernel as bf16 (no fp32 accumulators / casts)

@@ -274,7 +274,11 @@ int main(int argc, char** argv) {
     const int grid = 148;
     run<false, false, false, 128>("1cta SS  M128 N128 Bk", grid, mode);
     run<false, false, true, 128>("1cta SS  M128 N128 Bmn", grid, mode);
+    run<false, false, false, 64>("1cta SS  M128 N64 Bk", grid, mode);
+    run<false, false, true, 64>("1cta SS  M128 N64 Bmn", grid, mode);
+    run<false, true, true, 128>("1cta TS  M128 N128 Bmn", grid, mode);
     run<true, false, false, 128>("pair SS M256 N128 Bk", grid, mode);
+    run<true, false, false, 256>("pair SS M256 N256 Bk", grid, mode);
   }
   return 0;
 }
