@@ -46,6 +46,9 @@ constexpr float kLog2e = 1.4426950408889634f;
 #ifndef SA_BWD_POLY
 #define SA_BWD_POLY 0  // quads of every 8 whose exp2 runs on the FMA-pipe polynomial
 #endif
+#ifndef SA_BWD_PACKED
+#define SA_BWD_PACKED 0  // packed fp32x2 dS arithmetic (A/B)
+#endif
 
 struct BwdParams {
   CUtensorMap tq, tk, tv, tdo;   // bf16 [c, H, D], box 64 x 1 x 128
@@ -425,10 +428,18 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
           const float4 d4 = lds128f(dsum_a + (ch * 32 + e) * 4);
+#if SA_BWD_PACKED  // FADD2 / FMUL2: half the ALU issues of the dS arithmetic
+          float t0, t1, t2, t3, a0, a1, a2, a3;
+          add2(t0, t1, __uint_as_float(dr[e + 0]), __uint_as_float(dr[e + 1]), -d4.x, -d4.y);
+          add2(t2, t3, __uint_as_float(dr[e + 2]), __uint_as_float(dr[e + 3]), -d4.z, -d4.w);
+          mul2(a0, a1, pv[ch * 32 + e + 0], pv[ch * 32 + e + 1], t0, t1);
+          mul2(a2, a3, pv[ch * 32 + e + 2], pv[ch * 32 + e + 3], t2, t3);
+#else
           const float a0 = pv[ch * 32 + e + 0] * (__uint_as_float(dr[e + 0]) - d4.x);
           const float a1 = pv[ch * 32 + e + 1] * (__uint_as_float(dr[e + 1]) - d4.y);
           const float a2 = pv[ch * 32 + e + 2] * (__uint_as_float(dr[e + 2]) - d4.z);
           const float a3 = pv[ch * 32 + e + 3] * (__uint_as_float(dr[e + 3]) - d4.w);
+#endif
           dk[e / 2] = pack_bf16(a0, a1);
           dk[e / 2 + 1] = pack_bf16(a2, a3);
         }
