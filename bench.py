@@ -358,7 +358,18 @@ def measure(torch, dist, ring, _lib, q, k, v, dout, scale, layout, steps, warmup
     return ms, per, launches, rstats
 
 
-def roofline_block(per, steps, ms, hq, d, n_seq, world, peaks):
+def measured_traffic(config, world):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu
+    capture of the same configuration (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            rec = json.load(f).get("by_config", {}).get(f"{config}_n{world}")
+    except (OSError, ValueError):
+        return None
+    return rec
+
+
+def roofline_block(per, steps, ms, hq, d, n_seq, world, peaks, config):
     peak_burst = peaks.get("bf16_tflops", 1590.0)
     peak_sus = peaks.get("bf16_tflops_sustained", 1400.0)
     bwd_ms = statistics.mean(per["bwd_block"])
@@ -368,15 +379,12 @@ def roofline_block(per, steps, ms, hq, d, n_seq, world, peaks):
     pairs_per_launch = hq * n_seq * (n_seq + 1) / 2 / (world * world)
     bwd_achieved = 10.0 * d * pairs_per_launch / (bwd_ms / 1e3) / 1e12
     fwd_achieved = 4.0 * d * pairs_per_launch / (fwd_ms / 1e3) / 1e12
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f).get("bwd_block_bytes_per_launch")
-    except OSError:
-        pass
+    tr = measured_traffic(config, world) or {}
     return {"bound": "tensor", "kernel": "bwd_kernel (K5)", "achieved": bwd_achieved,
             "peak": peak_burst, "unit": "TFLOP/s", "frac": bwd_achieved / peak_burst,
-            "frac_of_sustained": bwd_achieved / peak_sus, "traffic": traffic,
+            "frac_of_sustained": bwd_achieved / peak_sus,
+            "traffic": tr.get("bwd_block_bytes_per_launch"),
+            "traffic_algorithmic_min": tr.get("bwd_block_algorithmic_bytes"),
             "peak_note": "MEASURED_PEAKS.json bf16_tflops (burst cuBLAS); frac_of_sustained "
                          "divides by bf16_tflops_sustained",
             "useful_flops_per_launch": 10.0 * d * pairs_per_launch,
@@ -451,7 +459,7 @@ def secondary_cfg2(torch, ring, _lib, dev, steps, peaks):
     ms, per, launches, _ = measure(torch, None, ring, _lib, q, k, v, dout, scale, "striped",
                                    max(steps, 10), 3, 1)
     total = useful_flops(s["seq"], s["hq"], s["d"])
-    roof = roofline_block(per, max(steps, 10), ms, s["hq"], s["d"], s["seq"], 1, peaks)
+    roof = roofline_block(per, max(steps, 10), ms, s["hq"], s["d"], s["seq"], 1, peaks, "cfg2")
     del q, k, v, dout
     return {"workload": s["desc"], "value": total / (ms / 1e3) / 1e12, "unit": "TFLOP/s",
             "ms_per_step": ms, "gpu_launches": launches,
@@ -575,7 +583,7 @@ def main():
                                "analytic_flop_weight_1": CM.tms(preset, n_seq, world, 1.0),
                                "analytic_flop_weight_2": CM.tms(preset, n_seq, world, 2.0)}
 
-    roofline = roofline_block(per, args.steps, ms, hq, d, n_seq, world, peaks)
+    roofline = roofline_block(per, args.steps, ms, hq, d, n_seq, world, peaks, args.config)
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(torch, dist, args, q, k, v, dout, scale, total, world, dev)

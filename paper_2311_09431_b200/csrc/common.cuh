@@ -405,6 +405,64 @@ SA_DEV void ex2_poly2(float& y0, float& y1, float x0, float x1) {
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
+// ---- forward epilogue shared by fwd.cu (D = 64) and fwd_pair.cu (D = 128): merge one
+// block's result into the running (o_acc, lse) state of the ring steps so far -- the
+// reference's carry rules (attention.py:321-328) and finalize (331-336), -inf safe: a row
+// that attended no key in this block (lse_blk = -inf) keeps its state bit for bit.
+struct LseMerge {
+  float w_prev;   // weight of the carried o_acc
+  float s_blk;    // scale of this block's unnormalised O (weight / l)
+  float lse_new;  // merged log-sum-exp (natural log)
+};
+SA_DEV LseMerge lse_merge(float lse_blk, float inv_l, bool first, const float* lse_prev_ptr) {
+  LseMerge r{0.f, inv_l, lse_blk};
+  if (!first) {
+    const float lse_prev = *lse_prev_ptr;
+    const float mx = fmaxf(lse_prev, lse_blk);
+    if (mx == -INFINITY) {
+      r.w_prev = 1.f;
+      r.s_blk = 0.f;
+      r.lse_new = -INFINITY;
+    } else {
+      const float a = __expf(lse_prev - mx), bb = __expf(lse_blk - mx);
+      r.lse_new = mx + __logf(a + bb);
+      r.w_prev = a / (a + bb);
+      r.s_blk = bb / (a + bb) * inv_l;
+    }
+  }
+  return r;
+}
+// 32 consecutive output columns of one row: v = O * s_blk (+ w_prev * o_acc); written as
+// bf16 to `out_row` on the last ring step, else as fp32 back to `acc_row`.
+SA_DEV void merge_store32(const uint32_t* o, const LseMerge& mw, bool first, bool last,
+                          float* acc_row, __nv_bfloat16* out_row) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; i++) v[i] = __uint_as_float(o[i]) * mw.s_blk;
+  if (!first) {
+    const float4* src = reinterpret_cast<const float4*>(acc_row);
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const float4 a = src[i];
+      v[4 * i] += mw.w_prev * a.x;
+      v[4 * i + 1] += mw.w_prev * a.y;
+      v[4 * i + 2] += mw.w_prev * a.z;
+      v[4 * i + 3] += mw.w_prev * a.w;
+    }
+  }
+  if (last) {
+    uint4* dst = reinterpret_cast<uint4*>(out_row);
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+      dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                          pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+  } else {
+    float4* dst = reinterpret_cast<float4*>(acc_row);
+#pragma unroll
+    for (int i = 0; i < 8; i++) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  }
+}
+
 // Byte offset of 16-byte chunk `chunk` (0..7) of row `row` inside a SW128 panel.
 SA_DEV uint32_t sw128_off(uint32_t row, uint32_t chunk) {
   return row * 128u + ((chunk ^ (row & 7u)) << 4);

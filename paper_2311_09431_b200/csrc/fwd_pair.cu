@@ -340,58 +340,20 @@ fwd_pair_kernel(const __grid_constant__ PairParams p) {
       const float l_tot = (l0 > 0.f ? l0 * ex2(m0 - m_f) : 0.f) + (l1 > 0.f ? l1 * ex2(m1 - m_f) : 0.f);
       const bool live = x < p.c;
       const float lse_blk = l_tot > 0.f ? (m_f + __log2f(l_tot)) * kLn2 : -INFINITY;
-      const float inv_l = l_tot > 0.f ? 1.f / l_tot : 0.f;
-      float w_prev = 0.f, w_blk = 1.f, lse_new = lse_blk;
       const int64_t lse_idx = (int64_t)h * p.c + x;
-      if (!p.first && live) {
-        const float lse_prev = p.lse[lse_idx];
-        const float mx = fmaxf(lse_prev, lse_blk);
-        if (mx == -INFINITY) {
-          w_prev = 1.f;
-          w_blk = 0.f;
-          lse_new = -INFINITY;
-        } else {
-          const float a = __expf(lse_prev - mx), bb = __expf(lse_blk - mx);
-          lse_new = mx + __logf(a + bb);
-          w_prev = a / (a + bb);
-          w_blk = bb / (a + bb);
-        }
-      }
-      const float s_blk = w_blk * inv_l;
+      const LseMerge mw = lse_merge(lse_blk, l_tot > 0.f ? 1.f / l_tot : 0.f, p.first || !live,
+                                    p.lse + lse_idx);
       const int64_t row_off = ((int64_t)x * p.hq + h) * D + grp * 64;
 #pragma unroll 1
-      for (int ch = 0; ch < 2; ch++) {
+      for (int ch = 0; ch < 2; ch++) {  // this group's half of the D columns
         uint32_t o[32];
         SA_TMEM_LD32(t_o + grp * 64 + ch * 32, o);
         tmem_ld_wait();
-        if (!live) continue;
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; i++) v[i] = __uint_as_float(o[i]) * s_blk;
-        if (!p.first) {
-          const float4* src = reinterpret_cast<const float4*>(p.o_acc + row_off + ch * 32);
-#pragma unroll
-          for (int i = 0; i < 8; i++) {
-            const float4 a = src[i];
-            v[4 * i] += w_prev * a.x;
-            v[4 * i + 1] += w_prev * a.y;
-            v[4 * i + 2] += w_prev * a.z;
-            v[4 * i + 3] += w_prev * a.w;
-          }
-        }
-        if (p.last) {
-          uint4* dst = reinterpret_cast<uint4*>(p.out + row_off + ch * 32);
-#pragma unroll
-          for (int i = 0; i < 4; i++)
-            dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                                pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
-        } else {
-          float4* dst = reinterpret_cast<float4*>(p.o_acc + row_off + ch * 32);
-#pragma unroll
-          for (int i = 0; i < 8; i++) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
+        if (live)
+          merge_store32(o, mw, p.first, p.last, p.o_acc + row_off + ch * 32,
+                        p.out + row_off + ch * 32);
       }
-      if (live && grp == 0) p.lse[lse_idx] = lse_new;
+      if (live && grp == 0) p.lse[lse_idx] = mw.lse_new;
     }
     if (p.tiles && warp == 4 && lane == 0) atomicAdd(p.tiles, (unsigned long long)n_mine);
   }
