@@ -699,6 +699,24 @@ def run_virtual_ring(args):
             "useful_tflops_striped_per_gpu_equiv":
                 useful_flops(n_seq, hq, d) / n / (res["striped"]["critical_path_ms"] / 1e3) / 1e12,
             "csv": args.csv or None, "clocks": clk.summary()}
+    # training-step speedup (TMS) from these measured per-layer critical
+    # paths + the layer's non-attention FLOPs at the measured sustained GEMM rate, beside
+    # the reference's analytic model (costmodel.py:109-128)
+    from paper_2311_09431_b200 import costmodel as CM
+    preset = next((m for m in CM.PRESETS.values() if m.n_head == hq and m.head_dim == d), None)
+    if preset is not None:
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                gemm = json.load(f).get("bf16_tflops_sustained", 1400.0)
+        except OSError:
+            gemm = 1400.0
+        mt = CM.measured_tms(preset, c, res["ring"]["critical_path_ms"],
+                             res["striped"]["critical_path_ms"], gemm)
+        line["tms"] = {"model": preset.name, "measured": mt.tms, "other_ms_per_layer": mt.other_ms,
+                       "analytic_flop_weight_1": CM.tms(preset, n_seq, n, 1.0),
+                       "analytic_flop_weight_2": CM.tms(preset, n_seq, n, 2.0),
+                       "note": "GQA kv heads are not modelled by the preset" if hkv != hq
+                       else None}
     print(json.dumps(line), flush=True)
 
 
