@@ -112,6 +112,24 @@ def test_c_abi_rejects_bad_arguments_without_launching():
     assert lib.sa_fwd_block(16, 16, 16, None, 16, 24, 128, 2, 2, 128, 0.1, 2, 1, 1, None, None) > 0
     assert lib.sa_bwd_block(16, 16, 16, 16, 16, 16, 16, 20, 16, 128, 2, 2, 128, 0.1, 2, None) > 0
     assert b"aligned" in lib.sa_last_error()
+    # sa_bwd_block_ex: exactly one dK/dV pair, whole range for bf16 outputs, aligned rows
+    ex = lib.sa_bwd_block_ex
+    assert ex(16, 16, 16, 16, 16, 16, 16, None, None, None, None, 256, 2, 2, 128, 0.1, 2, 0, -1,
+              None, None) > 0
+    assert b"dk_acc" in lib.sa_last_error()
+    assert ex(16, 16, 16, 16, 16, 16, 16, 16, 16, 16, None, 256, 2, 2, 128, 0.1, 2, 0, -1,
+              None, None) > 0
+    assert ex(16, 16, 16, 16, 16, 16, 16, None, None, 16, 16, 256, 2, 2, 128, 0.1, 2, 128, -1,
+              None, None) > 0
+    assert b"whole key range" in lib.sa_last_error()
+    assert ex(16, 16, 16, 16, 16, 16, 16, 16, 16, None, None, 256, 2, 2, 128, 0.1, 2, 64, -1,
+              None, None) > 0
+    assert b"128-aligned" in lib.sa_last_error()
+    # copy / IPC helpers reject null arguments without touching the device
+    assert lib.sa_memcpy_async(None, 16, 64, None) > 0
+    assert lib.sa_ipc_mem_handle(None, None, None) > 0
+    assert lib.sa_ipc_event_open(None, None) > 0
+    assert lib.sa_event_record(None, None) > 0
 
 
 def test_product_has_no_cpu_fallback():
