@@ -72,6 +72,9 @@ def parse(argv=None):
     ap.add_argument("--seq", type=int, default=0, help="override the config's sequence length")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "ipc"],
                     help="N > 1: ring hop backend (NCCL P2P or CUDA-IPC copy engines)")
+    ap.add_argument("--fused", action="store_true",
+                    help="N > 1 with --comm ipc: fused rotation (no dK/dV hops; the kernels "
+                         "reduce-add into the owner's buffer through peer memory)")
     ap.add_argument("--virtual-ring", type=int, default=0,
                     help="time N virtual ranks on ONE GPU, per (rank, round) block")
     ap.add_argument("--csv", default="", help="--virtual-ring: write the stats CSV here")
@@ -206,6 +209,7 @@ def arm_config(args, world):
             "config": args.config, "seq": s["seq"], "tokens_per_rank": c, "heads_q": s["hq"],
             "heads_kv": s["hkv"], "d_head": s["d"], "layout": "striped",
             "parallelism": f"sp{world}", "comm": args.comm if world > 1 else None,
+            "fused_dkv": bool(args.fused and world > 1),
             "l2": "inputs >= 1 GiB per rank > 126 MB L2, no flush",
             "useful_flops_per_step": useful_flops(s["seq"], s["hq"], s["d"])}
 
@@ -242,12 +246,15 @@ def _free_port():
     return p
 
 
+SHARE_GPU = os.environ.get("SA_BENCH_SHARE_GPU") == "1"
+
+
 def self_launch(args):
     """--gpus N > 1 outside torchrun: re-run under torch.distributed.run with N ranks."""
     if args.impl == "ours":
         import torch
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and not SHARE_GPU:
             print(json.dumps({"error": f"--gpus {args.gpus} but only {have} GPU(s) visible"}),
                   flush=True)
             sys.exit(2)
@@ -316,7 +323,7 @@ def timed_ops_class(ring, torch):
 
 
 def measure(torch, dist, ring, _lib, q, k, v, dout, scale, layout, steps, warmup, world,
-            comm=None, stats=False):
+            comm=None, stats=False, fused=False):
     """Time `steps` fwd+bwd steps (after `warmup`); returns (ms/step on this rank,
     per-kernel ms lists, launches, RingStats of the last step or None)."""
     TimedOps = timed_ops_class(ring, torch)
@@ -327,7 +334,8 @@ def measure(torch, dist, ring, _lib, q, k, v, dout, scale, layout, steps, warmup
         out, lse = ring.ring_forward(q, k, v, layout=layout, softmax_scale=scale, block_ops=bops,
                                      workspace=ws, comm=comm, stats=st)
         ring.ring_backward(dout, q, k, v, out, lse, layout=layout, softmax_scale=scale,
-                           block_ops=bops, workspace=ws, comm=comm, stats=st)
+                           block_ops=bops, workspace=ws, comm=comm, stats=st,
+                           fused_dkv=fused and world > 1)
 
     for _ in range(warmup):
         step()
@@ -490,12 +498,25 @@ def main():
     from paper_2311_09431_b200 import _lib, ring
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARE_GPU and world > 1:
+        # TEST MODE (SA_BENCH_SHARE_GPU=1): every rank on GPU 0, gloo for the host-side
+        # collectives, the copy-engine IPC hop (NCCL cannot put two ranks on one GPU).  It
+        # exercises the N > 1 code path end to end; its timings are of ranks time-sharing
+        # one GPU and mean nothing.
+        if args.comm != "ipc":
+            print(json.dumps({"error": "SA_BENCH_SHARE_GPU needs --comm ipc"}), flush=True)
+            sys.exit(2)
+        local = 0
+        args.no_e2e = True
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")
-        dist.init_process_group("nccl", device_id=dev)
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         if args.comm == "ipc":
             from paper_2311_09431_b200 import ipc
             comm = ipc.IpcComm()
@@ -516,7 +537,7 @@ def main():
     with ClockSampler(local) as clk:
         ms, per, launches, rstats = measure(torch, dist, ring, _lib, q, k, v, dout, scale,
                                             "striped", args.steps, args.warmup, world, comm,
-                                            stats=True)
+                                            stats=True, fused=args.fused)
     t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -566,7 +587,8 @@ def main():
     ring_cmp = None
     if world > 1 and not args.no_ring_compare:
         ms_r, per_r, _, _ = measure(torch, dist, ring, _lib, q, k, v, dout, scale, "ring",
-                                    args.steps, max(1, args.warmup), world, comm)
+                                    args.steps, max(1, args.warmup), world, comm,
+                                    fused=args.fused)
         tr = torch.tensor([ms_r], device=dev)
         dist.all_reduce(tr, op=dist.ReduceOp.MAX)
         ring_cmp = {"ring_ms_per_step": float(tr.item()),

@@ -62,6 +62,35 @@ def test_long_block_shortest_first_order_deterministic():
         assert (x.float() - z.float()).abs().max().item() <= 1e-2
 
 
+@pytest.mark.parametrize("layout", ["striped", "ring"])
+def test_serial_and_threaded_executors_bit_identical(layout):
+    """The reference's serial vs threaded executors give bit-identical outputs
+    (pkg/tests/test_simulator.py:198-207): here the serial executor is
+    ring.virtual_ring_forward (all ranks' rounds in order on one stream) and the threaded
+    one is ring_forward over LocalComm threads (side streams, copy-engine hops)."""
+    from paper_2311_09431_b200 import ring
+    n_dev, n, hq, hkv, d = 4, 2048, 4, 2, 128
+    q, k, v, _ = _inputs(n, hq, hkv, d, 13)
+    scale = 1 / math.sqrt(d)
+    scheme = R.STRIPED if layout == "striped" else R.CONTIGUOUS
+    rows = [torch.tensor(R.device_globals(scheme, n, n_dev, j), device="cuda")
+            for j in range(n_dev)]
+    st = lambda x: [x[r].contiguous() for r in rows]
+    outs, lses, _ = ring.virtual_ring_forward(st(q), st(k), st(v), layout=layout,
+                                              softmax_scale=scale)
+
+    def rank_fn(rank, comm):
+        o, lse = ring.ring_forward(st(q)[rank], st(k)[rank], st(v)[rank], layout=layout,
+                                   softmax_scale=scale, comm=comm)
+        torch.cuda.current_stream().synchronize()
+        return o.clone(), lse.clone()
+
+    res = ring.run_local_ring(n_dev, rank_fn, devices=["cuda:0"] * n_dev, timeout=120.0)
+    torch.cuda.synchronize()
+    for j, (o, lse) in enumerate(res):
+        assert torch.equal(o, outs[j]) and torch.equal(lse, lses[j])
+
+
 def test_threaded_ring_deterministic_reruns_bit_identical():
     from paper_2311_09431_b200 import ring
     n_dev, n, hq, hkv, d = 4, 4096, 4, 2, 128
