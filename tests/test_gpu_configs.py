@@ -179,3 +179,15 @@ def test_config1_gqa_32k_all_rows():
 def test_headline_256k_32heads_fwd_bwd_all_rows():
     """The metric's shape (configs[2]: seq 256k, 32 heads, d 128) at N = 1."""
     _run_block_and_check(262144, 32, 32, 128, heads=[0, 31], seed=33)
+
+
+def test_config3_512k_gqa_one_kv_group_all_rows():
+    """configs[3] (Llama-3-8B GQA 32 q / 8 kv heads, seq 512k) at N = 1: every row of a
+    whole kv group (q heads 0-3) incl. its summed dK / dV."""
+    _run_block_and_check(524288, 32, 8, 128, heads=[0, 1, 2, 3], seed=34)
+
+
+def test_config4_786k_long_sequence_all_rows():
+    """configs[4]'s sequence length (786k) at N = 1 with 8 of its 64 heads (the kernels'
+    per-head work does not depend on the head count): rows of heads 0 and 7."""
+    _run_block_and_check(786432, 8, 8, 128, heads=[0, 7], seed=35)
