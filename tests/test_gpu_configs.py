@@ -181,6 +181,36 @@ def test_headline_256k_32heads_fwd_bwd_all_rows():
     _run_block_and_check(262144, 32, 32, 128, heads=[0, 31], seed=33)
 
 
+@pytest.mark.parametrize("layout", ["striped", "ring"])
+def test_headline_256k_eight_rank_ring_equals_single_block(layout):
+    """configs[2]'s N = 8 schedule at full length (256k, c = 32768 per rank; 4 heads): all
+    64 (rank, round) blocks with their masks, LSE merges and travelling dK / dV
+    accumulators (the serial executor) reproduce the N = 1 block -- which the test above
+    checks row by row against the fp32 restatement -- after unpermuting (attention commutes
+    with the stripe permutation, pkg/tests/test_layout.py:106-125)."""
+    from paper_2311_09431_b200 import Layout, ring
+    n, h, d, n_dev = 262144, 4, 128, 8
+    gen = torch.Generator(device="cuda").manual_seed(36)
+    q, k, v, do = (torch.randn(n, h, d, device="cuda", generator=gen).bfloat16()
+                   for _ in range(4))
+    scale = 1.0 / math.sqrt(d)
+    out1, lse1 = ring.ring_forward(q, k, v, softmax_scale=scale)
+    g1 = ring.ring_backward(do, q, k, v, out1, lse1, softmax_scale=scale)
+    lay = Layout("striped" if layout == "striped" else "contiguous", n, n_dev)
+    c = n // n_dev
+    sh = lambda x: [s.contiguous() for s in lay.permute(x).split(c)]
+    qs, ks, vs, dos = sh(q), sh(k), sh(v), sh(do)
+    outs, lses, _ = ring.virtual_ring_forward(qs, ks, vs, layout=layout, softmax_scale=scale)
+    gs = ring.virtual_ring_backward(dos, qs, ks, vs, outs, lses, layout=layout,
+                                    softmax_scale=scale)
+    torch.cuda.synchronize()
+    _check(lay.gather(outs), out1.float(), "out")
+    lse8 = lay.gather([x.t().contiguous() for x in lses]).t()
+    assert (lse8 - lse1).abs().max().item() <= LSE_ABS
+    for name, got, want in zip(("dq", "dk", "dv"), gs, g1):
+        _check(lay.gather(got), want.float(), name)
+
+
 def test_config3_512k_gqa_one_kv_group_all_rows():
     """configs[3] (Llama-3-8B GQA 32 q / 8 kv heads, seq 512k) at N = 1: every row of a
     whole kv group (q heads 0-3) incl. its summed dK / dV."""
