@@ -15,6 +15,23 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
 
 
+@pytest.fixture(autouse=True)
+def _release_gpu_memory(request):
+    """After every GPU test, hand the caching allocator's free blocks back to the driver:
+    the full-size config tests hold tens of GB, and the multi-process tests that follow
+    start their own CUDA contexts on the same GPU."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import gc
+
+    import torch
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        gc.collect()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
+
 @pytest.fixture(scope="session")
 def tables():
     with open(os.path.join(GOLDEN, "tables.json")) as f:

@@ -80,9 +80,21 @@ def test_ipc_ring_processes_on_one_gpu(world, layout, fused):
     procs = [ctx.Process(target=_worker, args=(r, world, port, layout, n, hq, hkv, d, out_q,
                                                fused))
              for r in range(world)]
+    torch.cuda.empty_cache()  # the children open their own contexts on this GPU
     for p in procs:
         p.start()
-    results = [out_q.get(timeout=300) for _ in range(world)]
+    results = []
+    waited = 0.0
+    while len(results) < world:
+        try:
+            results.append(out_q.get(timeout=2.0))
+        except Exception:  # queue.Empty: fail fast if a rank died instead of hanging
+            waited += 2.0
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            if dead or waited > 300:
+                for p in procs:
+                    p.kill()
+                pytest.fail(f"IPC ranks failed (exit codes {dead}) or timed out")
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
