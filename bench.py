@@ -404,7 +404,7 @@ def roofline_block(per, steps, ms, hq, d, n_seq, world, peaks, config):
                            "useful_flops_per_launch": 4.0 * d * pairs_per_launch}}
 
 
-def run_e2e(torch, dist, args, q, k, v, dout, scale, total, world, dev):
+def run_e2e(torch, dist, args, q, k, v, dout, scale, total, world, dev, comm=None):
     """End to end through the public host API (paper_2311_09431_b200.host): inputs start in
     pinned host memory, results end in pinned host memory; the H2D / D2H copies are in the
     timed region (overlapped with compute across head groups by the API itself)."""
@@ -432,7 +432,8 @@ def run_e2e(torch, dist, args, q, k, v, dout, scale, total, world, dev):
 
     def e2e_step():
         ev = attention_fwd_bwd_host(hq_h, hk_h, hv_h, hdo_h, hout, hlse, hdq, hdk, hdv,
-                                    layout="striped", softmax_scale=scale, head_groups=groups)
+                                    layout="striped", softmax_scale=scale, head_groups=groups,
+                                    comm=comm)
         torch.cuda.current_stream().wait_event(ev)
 
     n_e2e = max(2, min(args.steps, 5))
@@ -507,7 +508,6 @@ def main():
             print(json.dumps({"error": "SA_BENCH_SHARE_GPU needs --comm ipc"}), flush=True)
             sys.exit(2)
         local = 0
-        args.no_e2e = True
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
@@ -609,7 +609,7 @@ def main():
     roofline = roofline_block(per, args.steps, ms, hq, d, n_seq, world, peaks, args.config)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(torch, dist, args, q, k, v, dout, scale, total, world, dev)
+        e2e = run_e2e(torch, dist, args, q, k, v, dout, scale, total, world, dev, comm)
     del q, k, v, dout
     torch.cuda.empty_cache()
     secondary = None

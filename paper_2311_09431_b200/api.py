@@ -47,44 +47,51 @@ def _scale(q, softmax_scale):
     return 1.0 / math.sqrt(q.shape[-1]) if softmax_scale is None else float(softmax_scale)
 
 
-def striped_attn_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale=None):
+def striped_attn_forward(q, k, v, *, group=None, layout: str = "striped", softmax_scale=None,
+                         comm=None):
     """Forward over the ring of ``group`` (default: the world, or one GPU when
-    torch.distributed is not initialised).  Returns (out, lse)."""
+    torch.distributed is not initialised).  ``comm``: the ring hop backend
+    (``ring.NcclComm`` by default, ``ipc.IpcComm``, ``ring.LocalComm``).  Returns (out, lse)."""
     _check(q, k, v, layout)
     scale = _scale(q, softmax_scale)
     if q.dim() == 4:
         res = [striped_attn_forward(q[b], k[b], v[b], group=group, layout=layout,
-                                    softmax_scale=scale) for b in range(q.shape[0])]
+                                    softmax_scale=scale, comm=comm) for b in range(q.shape[0])]
         return torch.stack([r[0] for r in res]), torch.stack([r[1] for r in res])
     return ring.ring_forward(q.contiguous(), k.contiguous(), v.contiguous(), group=group,
-                             layout=layout, softmax_scale=scale)
+                             layout=layout, softmax_scale=scale, comm=comm)
 
 
 def striped_attn_backward(dout, q, k, v, out, lse, *, group=None, layout: str = "striped",
-                          softmax_scale=None, deterministic: bool = False):
+                          softmax_scale=None, deterministic: bool = False, comm=None,
+                          fused_dkv: bool = False):
     """Backward -> (dq, dk, dv), bf16, same layout as the inputs.  ``deterministic``:
-    bit-identical reruns (ordered dQ reduction; slower)."""
+    bit-identical reruns (ordered dQ reduction; slower).  ``fused_dkv`` (peer-memory comms
+    only): no dK/dV hops, every rank's kernel adds into the held stripe's home buffer."""
     _check(q, k, v, layout)
     scale = _scale(q, softmax_scale)
     if q.dim() == 4:
         res = [striped_attn_backward(dout[b], q[b], k[b], v[b], out[b], lse[b], group=group,
                                      layout=layout, softmax_scale=scale,
-                                     deterministic=deterministic)
+                                     deterministic=deterministic, comm=comm,
+                                     fused_dkv=fused_dkv)
                for b in range(q.shape[0])]
         return tuple(torch.stack([r[i] for r in res]) for i in range(3))
     return ring.ring_backward(dout.contiguous(), q.contiguous(), k.contiguous(), v.contiguous(),
                               out.contiguous(), lse.contiguous(), group=group, layout=layout,
-                              softmax_scale=scale, deterministic=deterministic)
+                              softmax_scale=scale, deterministic=deterministic, comm=comm,
+                              fused_dkv=fused_dkv)
 
 
 class StripedAttnFunction(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, q, k, v, group, layout, softmax_scale, deterministic=False):
+    def forward(ctx, q, k, v, group, layout, softmax_scale, deterministic=False, comm=None,
+                fused_dkv=False):
         out, lse = striped_attn_forward(q, k, v, group=group, layout=layout,
-                                        softmax_scale=softmax_scale)
+                                        softmax_scale=softmax_scale, comm=comm)
         ctx.save_for_backward(q, k, v, out, lse)
         ctx.group, ctx.layout, ctx.softmax_scale = group, layout, softmax_scale
-        ctx.deterministic = deterministic
+        ctx.deterministic, ctx.comm, ctx.fused_dkv = deterministic, comm, fused_dkv
         return out
 
     @staticmethod
@@ -92,19 +99,21 @@ class StripedAttnFunction(torch.autograd.Function):
         q, k, v, out, lse = ctx.saved_tensors
         dq, dk, dv = striped_attn_backward(dout.contiguous(), q, k, v, out, lse, group=ctx.group,
                                            layout=ctx.layout, softmax_scale=ctx.softmax_scale,
-                                           deterministic=ctx.deterministic)
-        return dq, dk, dv, None, None, None, None
+                                           deterministic=ctx.deterministic, comm=ctx.comm,
+                                           fused_dkv=ctx.fused_dkv)
+        return dq, dk, dv, None, None, None, None, None, None
 
 
 def striped_attention(q, k, v, group=None, layout: str = "striped", softmax_scale=None,
-                      deterministic: bool = False):
+                      deterministic: bool = False, comm=None, fused_dkv: bool = False):
     """Autograd entry point: returns O for this rank's stripe."""
-    return StripedAttnFunction.apply(q, k, v, group, layout, softmax_scale, deterministic)
+    return StripedAttnFunction.apply(q, k, v, group, layout, softmax_scale, deterministic, comm,
+                                     fused_dkv)
 
 
-def ring_attention(q, k, v, group=None, softmax_scale=None):
+def ring_attention(q, k, v, group=None, softmax_scale=None, comm=None):
     """Contiguous-layout baseline (the ring the paper compares against)."""
-    return StripedAttnFunction.apply(q, k, v, group, "ring", softmax_scale)
+    return StripedAttnFunction.apply(q, k, v, group, "ring", softmax_scale, False, comm, False)
 
 
 def stripe_permute(x: torch.Tensor, n_devices: int, layout: str = "striped",

@@ -64,7 +64,7 @@ def ramp_groups(hq: int, hkv: int, max_groups: int = 16) -> list:
 
 def attention_fwd_bwd_host(q, k, v, dout, out, lse, dq, dk, dv, *, group=None,
                            layout: str = "striped", softmax_scale=None, head_groups=4,
-                           device=None):
+                           device=None, comm=None):
     """Forward + backward of this rank's stripe from/to pinned host memory.
 
     q, dout, out, dq: [c, Hq, D] bf16 pinned; k, v, dk, dv: [c, Hkv, D] bf16 pinned;
@@ -93,11 +93,11 @@ def attention_fwd_bwd_host(q, k, v, dout, out, lse, dq, dk, dv, *, group=None,
         torch.device(device)
     with torch.cuda.device(dev):  # copies and kernels go to the current device
         return _stream_groups(q, k, v, dout, out, lse, dq, dk, dv, sizes, r, c, d, scale, dev,
-                              group, layout)
+                              group, layout, comm)
 
 
 def _stream_groups(q, k, v, dout, out, lse, dq, dk, dv, sizes, r, c, d, scale, dev, group,
-                   layout):
+                   layout, comm=None):
     st = _streamer(dev)
     compute = torch.cuda.current_stream(dev)
     h2d, d2h = st.h2d, st.d2h
@@ -131,13 +131,13 @@ def _stream_groups(q, k, v, dout, out, lse, dq, dk, dv, sizes, r, c, d, scale, d
             compute.wait_event(st.copied[b])
         ws = st.work[b]
         o_g, lse_g = ring.ring_forward(s["q"], s["k"], s["v"], group=group, layout=layout,
-                                       softmax_scale=scale, workspace=ws)
+                                       softmax_scale=scale, workspace=ws, comm=comm)
         fwd_done = torch.cuda.Event()
         fwd_done.record(compute)
         compute.wait_event(bwd_in)
         dq_g, dk_g, dv_g = ring.ring_backward(s["do"], s["q"], s["k"], s["v"], o_g, lse_g,
                                               group=group, layout=layout, softmax_scale=scale,
-                                              workspace=ws)
+                                              workspace=ws, comm=comm)
         done = torch.cuda.Event()
         done.record(compute)
         st.freed[b] = done

@@ -34,5 +34,6 @@ def test_bench_two_ranks_shared_gpu(extra):
     sr = line["striped_vs_ring"]
     assert sr is not None and sr["ring_ms_per_step"] > 0 and "tms" in sr
     assert line["rank_imbalance"]["max"] >= 1.0
+    assert line["e2e"]["value"] > 0 and line["e2e"]["h2d_bytes_per_step"] > 0
     comm = line["comm"]
     assert comm["backend"] == "ipc" and comm["kv_hop_bytes"] == 2 * 4096 * 32 * 128 * 2
