@@ -21,7 +21,6 @@ from __future__ import annotations
 import ctypes
 import itertools
 import pickle
-import time
 from datetime import timedelta
 
 import torch
@@ -51,7 +50,7 @@ class IpcComm(Comm):
     name = "ipc"
     peer_memory = True
 
-    def __init__(self, group=None, store=None, timeout: float = STALL_TIMEOUT_S):
+    def __init__(self, group=None, store=None, timeout: float = 20 * STALL_TIMEOUT_S):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -59,8 +58,10 @@ class IpcComm(Comm):
         self.next_rank = (self.rank + 1) % self.world
         self.prev_rank = (self.rank - 1) % self.world
         self.next, self.prev = glob(self.next_rank), glob(self.prev_rank)
+        # the default store's own timeout is left alone (NCCL init and torch.distributed
+        # use it); every wait here carries its own.  Default 10 min: a rank's host can lag
+        # its peers by whole rounds of GPU work (seconds each at 786k) when it synchronises.
         self.store = store if store is not None else dist.distributed_c10d._get_default_store()
-        self.store.set_timeout(timedelta(seconds=timeout))
         self.timeout = timeout
         self.prefix = f"sa_ipc/{next(_instances)}/"
         self.seq = 0
@@ -84,21 +85,24 @@ class IpcComm(Comm):
         self._check(self._lib.sa_ipc_event_create(ctypes.byref(ev), h), "sa_ipc_event_create")
         return ev, _handle_bytes(h)
 
-    def _get(self, key):
-        t0 = time.monotonic()
+    def _fetch(self, key):
+        """The value of `key` once a peer has set it (bounded wait: the reference's
+        'ring channel stalled', simulator.py:40)."""
         try:
-            v = self.store.get(key)
+            self.store.wait([key], timedelta(seconds=self.timeout))
         except Exception as e:  # noqa: BLE001 - store timeout
             raise RuntimeError(f"ring channel stalled (rank {self.rank}, {key}): {e}") from e
-        if time.monotonic() - t0 > self.timeout:
-            raise RuntimeError(f"ring channel stalled (rank {self.rank})")
+        return self.store.get(key)
+
+    def _get(self, key):
+        v = self._fetch(key)
         self.store.delete_key(key)
         return v
 
     def _peer_event(self, rank, which):
         key = (rank, which)
         if key not in self._peer_ev:
-            handles = pickle.loads(self.store.get(f"{self.prefix}ev/{rank}"))
+            handles = pickle.loads(self._fetch(f"{self.prefix}ev/{rank}"))
             h = (ctypes.c_char * _HANDLE).from_buffer_copy(handles[which])
             ev = ctypes.c_void_p()
             self._check(self._lib.sa_ipc_event_open(h, ctypes.byref(ev)), "sa_ipc_event_open")
@@ -156,11 +160,11 @@ class IpcComm(Comm):
         n = self._n
         self._n += 1
         self.store.set(f"{self.prefix}{tag}/{n}/{self.rank}", value)
-        out = [self.store.get(f"{self.prefix}{tag}/{n}/{j}") for j in range(self.world)]
+        out = [self._fetch(f"{self.prefix}{tag}/{n}/{j}") for j in range(self.world)]
         # nobody deletes a key before every rank has read it: acknowledge, then clean up
         self.store.set(f"{self.prefix}{tag}_ack/{n}/{self.rank}", b"1")
         for j in range(self.world):
-            self.store.get(f"{self.prefix}{tag}_ack/{n}/{j}")
+            self._fetch(f"{self.prefix}{tag}_ack/{n}/{j}")
         return out
 
     def peer_views(self, t):
@@ -188,13 +192,13 @@ class IpcComm(Comm):
         self.store.set(key(self.rank), b"1")
         for j in range(self.world):
             if j != self.rank:
-                self.store.get(key(j))
+                self._fetch(key(j))
                 self._check(self._lib.sa_stream_wait_event(stream, self._peer_event(j, 2)),
                             "sa_stream_wait_event")
         # the next record of any rank's sync event must follow every rank's wait on it
         self.store.set(f"{self.prefix}sync_ack/{n}/{self.rank}", b"1")
         for j in range(self.world):
-            self.store.get(f"{self.prefix}sync_ack/{n}/{j}")
+            self._fetch(f"{self.prefix}sync_ack/{n}/{j}")
 
     def close(self):
         for base in self._opened.values():
