@@ -94,7 +94,6 @@ int sa_bwd_block(const void* q, const void* k, const void* v, const void* dout, 
                  int32_t hq, int32_t hkv, int32_t d, float softmax_scale, int32_t mask_kind,
                  void* stream);
 
-/* dst_bf16[i] = bf16(src[i]) (finalises dq/dk/dv accumulators and skipped last steps). */
 /* sa_bwd_block restricted to the keys [key_row_begin, key_row_end) of the held stripe
  * (128-aligned; the end may be c): only those dK / dV rows and their dQ contributions.
  * The ring launches a block in parts so each part's dK / dV rows can travel to the next
@@ -129,6 +128,7 @@ int sa_bwd_block_ex(const void* q, const void* k, const void* v, const void* dou
                     int32_t d, float softmax_scale, int32_t mask_kind, int32_t key_row_begin,
                     int32_t key_row_end, int32_t* dq_semaphore, void* stream);
 
+/* dst_bf16[i] = bf16(src[i]) (finalises dq/dk/dv accumulators and skipped last steps). */
 int sa_cast_f32_bf16(const float* src, void* dst, int64_t n, void* stream);
 
 /* Strided host<->device row copy (cudaMemcpy2DAsync): `height` rows of `width` bytes,
