@@ -371,7 +371,11 @@ bool fwd_pair_enabled(int32_t d) {
 #if SA_PERF_TRACE
   static const bool off = getenv("SA_FWD_SINGLE") != nullptr;  // A/B against fwd.cu
 #else
+#ifdef SA_FWD_FORCE_SINGLE  // A/B build: the 1-CTA fwd_kernel<128> for D = 128
+  constexpr bool off = true;
+#else
   constexpr bool off = false;
+#endif
 #endif
   return d == 128 && !off;
 }
