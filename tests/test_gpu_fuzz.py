@@ -3,6 +3,7 @@ boundaries, GQA ratios, both head dims, every mask kind, carried state) through 
 and backward kernels against the CPU oracle."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -19,7 +20,9 @@ def rel_l2(a, b):
     return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-30))
 
 
-def _cases(n=40, seed=2024):
+def _cases(n=None, seed=2024):
+    # SA_FUZZ_N widens the sweep for an extended run (profiles/r02_fuzz_extended.log)
+    n = int(os.environ.get("SA_FUZZ_N", "40")) if n is None else n
     rng = np.random.default_rng(seed)
     cs = [127, 129, 255, 257, 383, 385, 511, 513, 640, 767, 769, 896]
     out = []

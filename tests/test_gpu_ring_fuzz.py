@@ -4,6 +4,7 @@ layout, and the backward variants (travelling accumulators / fused rotation /
 deterministic) -- every output against the fp64 dense oracle (north-star tolerance)."""
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -26,7 +27,7 @@ def _case(seed):
     return world, c, d, hq, hkv, layout, variant
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SA_RING_FUZZ_N", "12"))))
 def test_ring_fuzz(seed):
     from paper_2311_09431_b200 import ring
     world, c, d, hq, hkv, layout, variant = _case(seed)
