@@ -22,6 +22,12 @@
 // so the compute warpgroups run P(i+1) right after dS(i) while the tensor core works
 // through dQ(i), dK(i), dP(i+1): the two sides overlap instead of alternating.
 //
+// CTA pairs (SA_BWD_PAIR, default): the grid is launched in clusters of two adjacent key
+// tiles that walk the same query-tile sequence in lockstep.  Each Q_i / dO_i tile is read
+// from L2 once and multicast into both CTAs (each CTA issues one of the two D=128 panels);
+// a stage is reloaded once BOTH CTAs' MMAs released it (the release commits are multicast).
+// Halving the per-SM Q / dO fetches measured +3% on the backward at c = 64k.
+//
 // Warp groups (512 threads):
 //   WG0: warp 0 TMA producer (+ lse/dsum staging), warp 1 MMA issuer, warp 2 TMEM alloc.
 //   WG1 / WG2: compute, query columns [0,64) / [64,128) of each tile (two warps per SMSP).
@@ -45,6 +51,9 @@ constexpr float kLog2e = 1.4426950408889634f;
 #endif
 #ifndef SA_BWD_POLY
 #define SA_BWD_POLY 0  // quads of every 8 whose exp2 runs on the FMA-pipe polynomial
+#endif
+#ifndef SA_BWD_PAIR
+#define SA_BWD_PAIR 1  // clusters of two key tiles sharing multicast Q / dO loads (A/B: 0)
 #endif
 #ifndef SA_BWD_PACKED
 #define SA_BWD_PACKED 0  // packed fp32x2 dS arithmetic (A/B)
@@ -123,7 +132,7 @@ __device__ __forceinline__ void store_row_bf16(__nv_bfloat16* base, uint32_t t_r
   }
 }
 
-template <int D>
+template <int D, bool kPair>
 __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ BwdParams p) {
   using L = BwdSmem<D>;
   constexpr int kPanels = D / 64;
@@ -142,11 +151,19 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
   // Head-major order: the ~148 concurrent CTAs share one kv head, so that head's Q / dO
   // and its dq_acc rows (the reduce-add target) stay L2-resident.  Within a head, small j
   // (most query tiles) first (LPT).
-  const int g = blockIdx.x / p.n_j;
-  const int j = p.j_begin + blockIdx.x % p.n_j;
+  // kPair: clusters of two adjacent key tiles (2m, 2m+1) walk the SAME query tiles in
+  // lockstep, so each Q_i / dO_i tile is fetched from L2 once and multicast to both CTAs
+  // (issued by alternate CTAs).  The odd CTA's first tile (i = 2m) is fully masked, and an
+  // odd tile count gets a "ghost" partner that contributes nothing.
+  const int nj_grid = kPair ? (p.n_j + 1) & ~1 : p.n_j;
+  const int jj = blockIdx.x % nj_grid;
+  const int g = blockIdx.x / nj_grid;
+  const int j = p.j_begin + jj;
+  const bool ghost = kPair && jj >= p.n_j;
+  const uint32_t rank = kPair ? (jj & 1) : 0;
   const int group = p.hq / p.hkv;
   const bool causal = p.kind != SA_MASK_FULLY_UNMASKED;
-  const int i0 = causal ? j : 0;
+  const int i0 = causal ? (kPair ? j - static_cast<int>(rank) : j) : 0;
   const int n_i = p.n_t - i0;
   const int n_it = group * n_i;
 
@@ -158,6 +175,11 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
     mbar_init(&bar[B_P_READY], 256);
     mbar_init(&bar[B_DS_READY], 256);
     mbar_init(&bar[B_DQ_FREE], 128);
+    if (kPair) {  // both CTAs' MMAs must have released a Q / dO stage before its reload
+      mbar_init(&bar[B_Q_EMPTY], 2);
+      mbar_init(&bar[B_Q_EMPTY + 1], 2);
+      mbar_init(&bar[B_DO_EMPTY], 2);
+    }
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -166,7 +188,10 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
     prefetch_tmap(&p.tdq);
   }
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    cluster_sync();  // the partner's barriers are initialised before any multicast lands
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_base_s;
   const uint32_t t_st = tbase, t_dpt = tbase + 128, t_dv = tbase + 256, t_dk = tbase + 256 + D;
@@ -176,6 +201,11 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
     if (warp == 0) {
       // ---------------------------------------------------------- producer
       const uint64_t pol_kv = policy_evict_first(), pol_q = policy_evict_last();
+      // kPair: which multicast Q / dO loads this CTA issues for both (D=128: one panel each;
+      // D=64: whole tiles, alternating by iteration)
+      auto fetches = [&](int pn, int it) {
+        return kPanels == 2 ? pn == static_cast<int>(rank) : (it & 1) == static_cast<int>(rank);
+      };
       if (lane == 0) {
         mbar_arrive_expect_tx(&bar[B_KV_FULL], 2 * L::kTile);
         for (int pn = 0; pn < kPanels; pn++) {
@@ -194,9 +224,13 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         if (lane == 0) {
           SA_TR(21);
           mbar_arrive_expect_tx(&bar[B_Q_FULL + s], L::kTile);
-          for (int pn = 0; pn < kPanels; pn++)
-            tma_load_3d(smem + L::kQ + s * L::kTile + pn * kPanelBytes, &p.tq, &bar[B_Q_FULL + s],
-                        64 * pn, h, 128 * i, pol_q);
+          for (int pn = 0; pn < kPanels; pn++) {
+            uint8_t* dst = smem + L::kQ + s * L::kTile + pn * kPanelBytes;
+            if (!kPair)
+              tma_load_3d(dst, &p.tq, &bar[B_Q_FULL + s], 64 * pn, h, 128 * i, pol_q);
+            else if (fetches(pn, it))
+              tma_load_3d_mc(dst, &p.tq, &bar[B_Q_FULL + s], 64 * pn, h, 128 * i, pol_q, 3);
+          }
         }
 #pragma unroll
         for (int e = 0; e < 4; e++) {
@@ -216,10 +250,21 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         if (lane == 0) {
           SA_TR(22);
           mbar_arrive_expect_tx(&bar[B_DO_FULL], L::kTile);
-          for (int pn = 0; pn < kPanels; pn++)
-            tma_load_3d(smem + L::kDO + pn * kPanelBytes, &p.tdo, &bar[B_DO_FULL], 64 * pn, h,
-                        128 * i, pol_q);
+          for (int pn = 0; pn < kPanels; pn++) {
+            uint8_t* dst = smem + L::kDO + pn * kPanelBytes;
+            if (!kPair)
+              tma_load_3d(dst, &p.tdo, &bar[B_DO_FULL], 64 * pn, h, 128 * i, pol_q);
+            else if (fetches(pn, it))
+              tma_load_3d_mc(dst, &p.tdo, &bar[B_DO_FULL], 64 * pn, h, 128 * i, pol_q, 3);
+          }
         }
+      }
+      if (kPair) {
+        // consume the partner's last stage releases, so it cannot arrive on this CTA's
+        // barriers after this CTA has exited (the final cluster barrier orders the rest)
+        for (int it = n_it > 2 ? n_it - 2 : 0; it < n_it; it++)
+          mbar_wait(&bar[B_Q_EMPTY + (it & 1)], (it >> 1) & 1);
+        if (n_it > 0) mbar_wait(&bar[B_DO_EMPTY], (n_it - 1) & 1);
       }
     } else if (SA_PERF_TRACE && warp == 3 && lane == 0 && p.trace && blockIdx.x == p.trace_cta) {
       // perf experiments only: completion time of every MMA group, in issue order
@@ -304,7 +349,10 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
           for (int kk = 0; kk < 8; kk++)  // P^T: q cols [0,64) at TMEM [0,32), [64,128) at [64,96)
             mma_ts2(t_dv, t_st + (kk < 4 ? kk * 8 : 64 + (kk - 4) * 8), b + kk * 128, hi, id_kv,
                     (it > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&bar[B_DO_EMPTY]);
+          if (kPair)
+            mma_commit_mc(&bar[B_DO_EMPTY], 3);  // frees the stage in both CTAs' view
+          else
+            mma_commit(&bar[B_DO_EMPTY]);
         }
         __syncwarp();
         SA_TR(5);
@@ -324,7 +372,10 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
           for (int kk = 0; kk < 8; kk++)
             mma_ss2(t_dk, c + kmaj(kk), hi, e + kk * 128, hi, id_kv, (it > 0 || kk > 0) ? 1u : 0u);
           // one commit: Q stage s and the dS tile are both free once dK(it) retired
-          mma_commit(&bar[B_Q_EMPTY + s]);
+          if (kPair)
+            mma_commit_mc(&bar[B_Q_EMPTY + s], 3);
+          else
+            mma_commit(&bar[B_Q_EMPTY + s]);
         }
         __syncwarp();
         SA_TR(7);
@@ -345,7 +396,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
     for (int it = 0; it < n_it; it++) {
       const int s = it & 1;
       const int i = i0 + it % n_i;
-      const bool masked = (causal && i == j) || (i + 1) * 128 > p.c || (j + 1) * 128 > p.c;
+      const bool masked = (causal && i <= j) || (i + 1) * 128 > p.c || (j + 1) * 128 > p.c || ghost;
       const uint32_t lse_a = sbase + L::kLse + s * 512 + half * 256;
       const uint32_t dsum_a = sbase + L::kDsum + s * 512 + half * 256;
       const int xbase = 128 * i + 64 * half;
@@ -390,7 +441,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         if (masked) {
 #pragma unroll
           for (int e = 0; e < 32; e++)
-            if (!allowed_bwd(p.kind, xbase + ch * 32 + e, y, p.c)) pv[ch * 32 + e] = 0.f;
+            if (ghost || !allowed_bwd(p.kind, xbase + ch * 32 + e, y, p.c)) pv[ch * 32 + e] = 0.f;
         }
         uint32_t pk[16];
 #pragma unroll
@@ -454,7 +505,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       mbar_arrive(&bar[B_DS_READY]);
       if (tr) SA_TR(13);
     }
-    if (half == 0) {
+    if (half == 0 && !ghost) {
       // ---------------------------------------------------------- dV epilogue
       mbar_wait(&bar[B_KV_DONE], 0);
       tc_fence_after();
@@ -503,6 +554,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
       if (leader) SA_TR(18);
       if (SA_PERF_TRACE && (p.debug & 1)) continue;
       int* sem = p.dq_sem ? p.dq_sem + (int64_t)h * p.n_t + i : nullptr;
+      if (ghost || (causal && i < j)) continue;  // kPair's all-masked tiles: dQ is exactly 0
       if (sem && leader) {
         // deterministic dQ: the key tiles add into query tile i in ascending j order.  The
         // CTAs of lower j have lower blockIdx (scheduled earlier), so the wait cannot
@@ -513,6 +565,7 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
           if (++spins > (1u << 30)) __trap();
         fence_proxy_async_global();  // the previous adder's TMA writes before ours
       }
+      __syncwarp();  // reconverge warp 12 before the named barriers below
 #pragma unroll
       for (int ch = 0; ch < kChunks; ch++) {
         const uint32_t buf = sbase + L::kStg + (ch & 1) * kPanelBytes;
@@ -546,7 +599,9 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
     // ------------------------------------------------------------ dK epilogue
     mbar_wait(&bar[B_KV_DONE], 0);
     tc_fence_after();
-    if (p.dk_out) {
+    if (ghost) {
+      // the ghost partner owns no key rows
+    } else if (p.dk_out) {
       store_row_bf16<D>(p.dk_out, t_dk + lane_off, p.scale, 128 * j + static_cast<int>(row), g, p);
     } else {
     const uint32_t kst = sbase + L::kDO;  // dO + dS buffers (contiguous) are free now
@@ -574,20 +629,39 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (kPair)
+    cluster_sync();  // no CTA leaves while its partner's multicasts / commits may target it
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
 }
 
-template <int D>
+template <int D, bool kPair>
 int launch_bwd_d(BwdParams& prm, cudaStream_t st) {
   const int smem = BwdSmem<D>::kAlloc;
   static unsigned long long attr_devices = 0;
-  if (int r = set_smem_attr_once(bwd_kernel<D>, smem, &attr_devices)) return r;
-  bwd_kernel<D><<<prm.n_j * prm.hkv, 512, smem, st>>>(prm);
-  return check_launch("bwd_kernel");
+  if (int r = set_smem_attr_once(bwd_kernel<D, kPair>, smem, &attr_devices)) return r;
+  if (!kPair) {
+    bwd_kernel<D, false><<<prm.n_j * prm.hkv, 512, smem, st>>>(prm);
+    return check_launch("bwd_kernel");
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(((prm.n_j + 1) & ~1) * prm.hkv);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  (void)cudaLaunchKernelEx(&cfg, bwd_kernel<D, true>, prm);  // errors surface in check_launch
+  return check_launch("bwd_kernel(pair)");
 }
 
 }  // namespace
@@ -637,7 +711,11 @@ int launch_bwd(const void* q, const void* k, const void* v, const void* dout, co
     prm.trace_cta = atoi(tr);
   }
 #endif
-  int r = d == 128 ? launch_bwd_d<128>(prm, st) : launch_bwd_d<64>(prm, st);
+  int r;
+  if (SA_BWD_PAIR)
+    r = d == 128 ? launch_bwd_d<128, true>(prm, st) : launch_bwd_d<64, true>(prm, st);
+  else
+    r = d == 128 ? launch_bwd_d<128, false>(prm, st) : launch_bwd_d<64, false>(prm, st);
 #if SA_PERF_TRACE
   if (tr && r == 0) {
     long long h[16 * 32];
