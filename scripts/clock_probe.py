@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--c", type=int, default=65536)
 ap.add_argument("--h", type=int, default=32)
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--fwd", action="store_true", help="time the forward block instead")
 a = ap.parse_args()
 dev = "cuda"
 q, k, v, do = (torch.randn(a.c, a.h, 128, device=dev).bfloat16() for _ in range(4))
@@ -33,13 +34,19 @@ for _ in range(3):
     ops.bwd_block_final(q, k, v, do, lse, dsum, dq, dk, dv, s, 2)
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+step = (lambda: ops.fwd_block(q, k, v, None, lse, out, s, 2, True, True)) if a.fwd else \
+    (lambda: ops.bwd_block_final(q, k, v, do, lse, dsum, dq, dk, dv, s, 2))
+for _ in range(2):
+    step()
+torch.cuda.synchronize()
 with ClockSampler(0) as clk:
     e0.record()
     for _ in range(a.iters):
-        ops.bwd_block_final(q, k, v, do, lse, dsum, dq, dk, dv, s, 2)
+        step()
     e1.record()
     torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / a.iters
-flops = 10 * 128 * a.h * a.c * (a.c + 1) / 2
-print(f"bwd c={a.c} debug={os.environ.get('SA_BWD_DEBUG', '0')}: {ms:.3f} ms "
+flops = (4 if a.fwd else 10) * 128 * a.h * a.c * (a.c + 1) / 2
+dbg = os.environ.get("SA_FWD_DEBUG" if a.fwd else "SA_BWD_DEBUG", "0")
+print(f"{'fwd' if a.fwd else 'bwd'} c={a.c} debug={dbg}: {ms:.3f} ms "
       f"{flops / ms / 1e9:.1f} TFLOP/s  clocks {clk.summary()}")

@@ -46,10 +46,10 @@ def test_single_block_deterministic_reruns_bit_identical(n, hq, hkv, d):
             assert np.max(np.abs(got.float().cpu().numpy() - w)) <= 2e-2
 
 
-def test_long_block_shortest_first_order_deterministic():
-    """c = 64k with a GQA group of 2: the head's working set exceeds the L2 budget, so the
-    backward grid runs shortest-first and the ordered dQ reduce runs in descending key-tile
-    order -- still bit-identical reruns, and the same numbers as the unordered path."""
+def test_long_block_deterministic():
+    """c = 64k with a GQA group of 2 (512 key tiles = 256 CTA pairs per kv head, each CTA
+    walking both q heads): the ordered dQ reduce gives bit-identical reruns and the same
+    numbers as the unordered path."""
     from paper_2311_09431_b200 import api
     q, k, v, do = _inputs(65536, 2, 1, 128, 21)
     out, lse = api.striped_attn_forward(q, k, v)
