@@ -17,18 +17,21 @@ from paper_2311_09431_b200 import ops  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--c", type=int, default=65536)
 ap.add_argument("--h", type=int, default=32)
+ap.add_argument("--hkv", type=int, default=0)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--fwd", action="store_true", help="time the forward block instead")
 a = ap.parse_args()
 dev = "cuda"
-q, k, v, do = (torch.randn(a.c, a.h, 128, device=dev).bfloat16() for _ in range(4))
+hkv = a.hkv or a.h
+q, do = (torch.randn(a.c, a.h, 128, device=dev).bfloat16() for _ in range(2))
+k, v = (torch.randn(a.c, hkv, 128, device=dev).bfloat16() for _ in range(2))
 out = torch.empty_like(q)
 lse = torch.empty(a.h, a.c, device=dev)
 s = 1 / math.sqrt(128)
 ops.fwd_block(q, k, v, None, lse, out, s, 2, True, True)
 dsum = torch.empty(a.h, a.c, device=dev)
 dq = torch.empty(a.c, a.h, 128, device=dev)
-dk, dv = torch.empty_like(q), torch.empty_like(q)
+dk, dv = torch.empty_like(k), torch.empty_like(v)
 ops.bwd_preprocess(out, do, dsum, dq)
 for _ in range(3):
     ops.bwd_block_final(q, k, v, do, lse, dsum, dq, dk, dv, s, 2)
