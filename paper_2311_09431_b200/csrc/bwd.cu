@@ -151,10 +151,11 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
   // Head-major order: the ~148 concurrent CTAs share one kv head, so that head's Q / dO
   // and its dq_acc rows (the reduce-add target) stay L2-resident.  Within a head, small j
   // (most query tiles) first (LPT).
-  // kPair: clusters of two adjacent key tiles (2m, 2m+1) walk the SAME query tiles in
-  // lockstep, so each Q_i / dO_i tile is fetched from L2 once and multicast to both CTAs
-  // (issued by alternate CTAs).  The odd CTA's first tile (i = 2m) is fully masked, and an
-  // odd tile count gets a "ghost" partner that contributes nothing.
+  // kPair: clusters of two adjacent key tiles (j_begin + 2m, j_begin + 2m + 1) walk the
+  // SAME query tiles in lockstep, so each Q_i / dO_i tile is fetched from L2 once and
+  // multicast to both CTAs (each CTA issues half of the loads).  The odd CTA's first tile
+  // (i = j - 1) is fully masked, and an odd tile count gets a "ghost" partner that
+  // contributes nothing.
   const int nj_grid = kPair ? (p.n_j + 1) & ~1 : p.n_j;
   const int jj = blockIdx.x % nj_grid;
   const int g = blockIdx.x / nj_grid;
