@@ -181,18 +181,20 @@ def test_headline_256k_32heads_fwd_bwd_all_rows():
     _run_block_and_check(262144, 32, 32, 128, heads=[0, 31], seed=33)
 
 
+@pytest.mark.parametrize("n,hq,hkv", [(262144, 4, 4), (524288, 8, 2)])
 @pytest.mark.parametrize("layout", ["striped", "ring"])
-def test_headline_256k_eight_rank_ring_equals_single_block(layout):
-    """configs[2]'s N = 8 schedule at full length (256k, c = 32768 per rank; 4 heads): all
-    64 (rank, round) blocks with their masks, LSE merges and travelling dK / dV
-    accumulators (the serial executor) reproduce the N = 1 block -- which the test above
-    checks row by row against the fp32 restatement -- after unpermuting (attention commutes
-    with the stripe permutation, pkg/tests/test_layout.py:106-125)."""
+def test_headline_256k_eight_rank_ring_equals_single_block(layout, n, hq, hkv):
+    """configs[2]'s N = 8 schedule at full length (256k, c = 32768 per rank; 4 heads), and
+    configs[3]'s (512k, c = 65536, GQA 4:1 on 8 of its q heads): all 64 (rank, round)
+    blocks with their masks, LSE merges and travelling dK / dV accumulators (the serial
+    executor) reproduce the N = 1 block -- which the tests here check row by row against
+    the fp32 restatement -- after unpermuting (attention commutes with the stripe
+    permutation, pkg/tests/test_layout.py:106-125)."""
     from paper_2311_09431_b200 import Layout, ring
-    n, h, d, n_dev = 262144, 4, 128, 8
+    d, n_dev = 128, 8
     gen = torch.Generator(device="cuda").manual_seed(36)
-    q, k, v, do = (torch.randn(n, h, d, device="cuda", generator=gen).bfloat16()
-                   for _ in range(4))
+    q, do = (torch.randn(n, hq, d, device="cuda", generator=gen).bfloat16() for _ in range(2))
+    k, v = (torch.randn(n, hkv, d, device="cuda", generator=gen).bfloat16() for _ in range(2))
     scale = 1.0 / math.sqrt(d)
     out1, lse1 = ring.ring_forward(q, k, v, softmax_scale=scale)
     g1 = ring.ring_backward(do, q, k, v, out1, lse1, softmax_scale=scale)
