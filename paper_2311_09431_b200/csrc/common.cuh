@@ -422,6 +422,72 @@ SA_DEV void ex2_poly2(float& y0, float& y1, float x0, float x1) {
   y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
 }
 
+// ---- forward softmax of one S row (128 keys held by one thread), shared by fwd.cu and
+// fwd_pair.cu: the reference's tile fold (attention.py:310-328) in the exp2 domain.
+// Key column limit of a masked (diagonal and/or ragged) tile: keys >= the returned value
+// are masked -- inclusive y <= x, strict y < x (attention.py:155-183), ragged y < c.
+SA_DEV int key_limit(int kind, int x, int c, int j) {
+  const int last = kind == SA_MASK_CAUSAL_INCLUSIVE ? x + 1 : kind == SA_MASK_CAUSAL_EXCLUSIVE ? x : c;
+  return min(last, c) - j * 128;
+}
+// Keys >= lim of a masked tile -> -inf (before the row maximum).
+SA_DEV void mask_row(uint32_t (&r)[128], int lim) {
+#pragma unroll
+  for (int i = 0; i < 128; i++)
+    if (i >= lim) r[i] = __float_as_uint(-INFINITY);
+}
+// Row maximum of the raw scores.  Eight independent partial maxima: no 128-long
+// dependency chain (ptxas pairs them into FMNMX3).
+SA_DEV float s_row_max(const uint32_t (&r)[128]) {
+  float mx8[8];
+#pragma unroll
+  for (int u = 0; u < 8; u++) mx8[u] = __uint_as_float(r[u]);
+#pragma unroll
+  for (int i = 8; i < 128; i++) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(r[i]));
+  return fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+}
+// p = 2^(s * scale_log2 - m) (neg_m = -m, 0 for a row with no key yet), packed as bf16
+// pairs into r[0..63] for the PV MMA; returns the fp32 row sum of the unrounded p.  Pairs
+// go through FFMA2; kPoly of every 16 pairs take the FMA-pipe polynomial (the rest
+// MUFU.EX2) so the two pipes share the exponentials; four FADD2 chains for the sum.
+template <bool kMasked, int kPoly>
+SA_DEV float s_row_exp_pack(uint32_t (&r)[128], float scale_log2, float neg_m, int lim) {
+  float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 64; i++) {
+    float x0, x1, p0, p1;
+    fma2(x0, x1, __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), scale_log2,
+         scale_log2, neg_m, neg_m);
+    if ((i & 15) < kPoly) {
+      ex2_poly2(p0, p1, x0, x1);
+    } else {
+      p0 = ex2(x0);
+      p1 = ex2(x1);
+    }
+    if constexpr (kMasked) {
+      p0 = 2 * i < lim ? p0 : 0.f;
+      p1 = 2 * i + 1 < lim ? p1 : 0.f;
+    }
+    add2(sa[i & 3], sb[i & 3], sa[i & 3], sb[i & 3], p0, p1);
+    r[i] = pack_bf16(p0, p1);
+  }
+  return ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sb[0] + sb[1]) + (sb[2] + sb[3]));
+}
+// Lazy rescale of one thread's O row in TMEM (D fp32 columns) by `factor`.
+template <int D>
+SA_DEV void tmem_scale_row(uint32_t t_o, float factor) {
+#pragma unroll 1
+  for (int ch = 0; ch < D / 32; ch++) {
+    uint32_t o[32];
+    SA_TMEM_LD32(t_o + ch * 32, o);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+    SA_TMEM_ST32(t_o + ch * 32, o);
+  }
+}
+
 // ---- forward epilogue shared by fwd.cu (D = 64) and fwd_pair.cu (D = 128): merge one
 // block's result into the running (o_acc, lse) state of the ring steps so far -- the
 // reference's carry rules (attention.py:321-328) and finalize (331-336), -inf safe: a row

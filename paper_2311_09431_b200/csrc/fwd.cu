@@ -259,25 +259,9 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
       // Two instantiations so the common (unmasked) tile carries no per-element selects.
       auto tile = [&](auto masked_tag) {
         constexpr bool kMasked = decltype(masked_tag)::value;
-        int lim = 128;
-        if constexpr (kMasked) {
-          const int last = p.kind == SA_MASK_CAUSAL_INCLUSIVE   ? x + 1
-                           : p.kind == SA_MASK_CAUSAL_EXCLUSIVE ? x
-                                                                : p.c;
-          lim = min(last, p.c) - j * 128;
-#pragma unroll
-          for (int i = 0; i < 128; i++)
-            if (i >= lim) r[i] = __float_as_uint(-INFINITY);
-        }
-        // 8 independent partial maxima: no 128-long dependency chain
-        float mx8[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) mx8[u] = __uint_as_float(r[u]);
-#pragma unroll
-        for (int i = 8; i < 128; i++) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(r[i]));
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        const float mt = mx * p.scale_log2;
+        const int lim = kMasked ? key_limit(p.kind, x, p.c, j) : 128;
+        if constexpr (kMasked) mask_row(r, lim);
+        const float mt = s_row_max(r) * p.scale_log2;
         if (m == -INFINITY) {
           m = mt;
         } else if (mt > m + kRescaleThreshold) {
@@ -286,28 +270,8 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
           resc = true;
         }
         const float neg_m = (m == -INFINITY) ? 0.f : -m;
-        // p = 2^(s*scale*log2e - m): pairs through FFMA2; 7 of every 16 pairs take the
-        // FMA-pipe polynomial, the rest MUFU.EX2 (balances the two pipes); 4 FADD2 chains.
-        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int i = 0; i < 64; i++) {
-          float x0, x1, p0, p1;
-          fma2(x0, x1, __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), p.scale_log2,
-               p.scale_log2, neg_m, neg_m);
-          if ((i & 15) < (D == 64 ? SA_FWD_POLY_D64 : SA_FWD_POLY_D128)) {
-            ex2_poly2(p0, p1, x0, x1);
-          } else {
-            p0 = ex2(x0);
-            p1 = ex2(x1);
-          }
-          if constexpr (kMasked) {
-            p0 = 2 * i < lim ? p0 : 0.f;
-            p1 = 2 * i + 1 < lim ? p1 : 0.f;
-          }
-          add2(sa[i & 3], sb[i & 3], sa[i & 3], sb[i & 3], p0, p1);
-          r[i] = pack_bf16(p0, p1);
-        }
-        return ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sb[0] + sb[1]) + (sb[2] + sb[3]));
+        return s_row_exp_pack<kMasked, D == 64 ? SA_FWD_POLY_D64 : SA_FWD_POLY_D128>(
+            r, p.scale_log2, neg_m, lim);
       };
       const float sum = masked ? tile(std::true_type{}) : tile(std::false_type{});
       l = l * factor + sum;
@@ -316,15 +280,7 @@ __global__ void __launch_bounds__(384, 1) fwd_kernel(const __grid_constant__ Fwd
       if (__any_sync(0xffffffffu, resc) && j > 0) {
         mbar_wait(&o_done[t], (j - 1) & 1);
         tc_fence_after();
-#pragma unroll 1
-        for (int ch = 0; ch < D / 32; ch++) {
-          uint32_t o[32];
-          SA_TMEM_LD32(t_o + ch * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
-          SA_TMEM_ST32(t_o + ch * 32, o);
-        }
+        tmem_scale_row<D>(t_o, factor);
       }
       tmem_st_wait();
       tc_fence_before();

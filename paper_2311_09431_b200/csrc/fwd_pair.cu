@@ -233,21 +233,10 @@ fwd_pair_kernel(const __grid_constant__ PairParams p) {
         SA_TMEM_LD32(t_s + 96, (r + 96));
         tmem_ld_wait();
         if (masked) {
-          const int last = p.kind == SA_MASK_CAUSAL_INCLUSIVE   ? x + 1
-                           : p.kind == SA_MASK_CAUSAL_EXCLUSIVE ? x
-                                                                : p.c;
-          lim = min(last, p.c) - j * 128;
-#pragma unroll
-          for (int i = 0; i < 128; i++)
-            if (i >= lim) r[i] = __float_as_uint(-INFINITY);
+          lim = key_limit(p.kind, x, p.c, j);
+          mask_row(r, lim);
         }
-        float mx8[8];
-#pragma unroll
-        for (int u = 0; u < 8; u++) mx8[u] = __uint_as_float(r[u]);
-#pragma unroll
-        for (int i = 8; i < 128; i++) mx8[i & 7] = fmaxf(mx8[i & 7], __uint_as_float(r[i]));
-        mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        mx = s_row_max(r);
       }
       // running max hand-off: m_{j-1} from the other group, m_j to it
       float m_prev = -INFINITY;
@@ -275,30 +264,8 @@ fwd_pair_kernel(const __grid_constant__ PairParams p) {
       }
       if (live_tile) {
         const float neg_m = (m_new == -INFINITY) ? 0.f : -m_new;
-        auto tile = [&](auto masked_tag) {
-          constexpr bool kMasked = decltype(masked_tag)::value;
-          float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int i = 0; i < 64; i++) {
-            float x0, x1, p0, p1;
-            fma2(x0, x1, __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]), p.scale_log2,
-                 p.scale_log2, neg_m, neg_m);
-            if ((i & 15) < SA_FWD_POLY) {
-              ex2_poly2(p0, p1, x0, x1);
-            } else {
-              p0 = ex2(x0);
-              p1 = ex2(x1);
-            }
-            if constexpr (kMasked) {
-              p0 = 2 * i < lim ? p0 : 0.f;
-              p1 = 2 * i + 1 < lim ? p1 : 0.f;
-            }
-            add2(sa[i & 3], sb[i & 3], sa[i & 3], sb[i & 3], p0, p1);
-            r[i] = pack_bf16(p0, p1);
-          }
-          return ((sa[0] + sa[1]) + (sa[2] + sa[3])) + ((sb[0] + sb[1]) + (sb[2] + sb[3]));
-        };
-        l += masked ? tile(std::true_type{}) : tile(std::false_type{});
+        l += masked ? s_row_exp_pack<true, SA_FWD_POLY>(r, p.scale_log2, neg_m, lim)
+                    : s_row_exp_pack<false, SA_FWD_POLY>(r, p.scale_log2, neg_m, lim);
       } else {
 #pragma unroll
         for (int i = 0; i < 64; i++) r[i] = 0u;  // tile above this CTA's diagonal: P = 0
@@ -310,16 +277,7 @@ fwd_pair_kernel(const __grid_constant__ PairParams p) {
         // O holds PV(0..j-1) relative to m_prev: rescale once PV(j-1) has landed
         mbar_wait(&bar.pv_done[(j - 1) % kSt], ((j - 1) / kSt) & 1);
         tc_fence_after();
-        const float factor = resc ? ex2(m_prev - m_new) : 1.f;
-#pragma unroll 1
-        for (int ch = 0; ch < D / 32; ch++) {
-          uint32_t o[32];
-          SA_TMEM_LD32(t_o + ch * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; i++) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
-          SA_TMEM_ST32(t_o + ch * 32, o);
-        }
+        tmem_scale_row<D>(t_o, resc ? ex2(m_prev - m_new) : 1.f);
       }
       tmem_st_wait();
       tc_fence_before();
