@@ -448,9 +448,9 @@ SA_DEV float s_row_max(const uint32_t (&r)[128]) {
                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
 }
 // p = 2^(s * scale_log2 - m) (neg_m = -m, 0 for a row with no key yet), packed as bf16
-// pairs into r[0..63] for the PV MMA; returns the fp32 row sum of the unrounded p.  Pairs
-// go through FFMA2; kPoly of every 16 pairs take the FMA-pipe polynomial (the rest
-// MUFU.EX2) so the two pipes share the exponentials; four FADD2 chains for the sum.
+// pairs in place into r[0..63] for the PV MMA; returns the fp32 row sum of the unrounded
+// p.  Pairs go through FFMA2; kPoly of every 16 pairs take the FMA-pipe polynomial (the
+// rest MUFU.EX2) so the two pipes share the exponentials; four FADD2 chains for the sum.
 template <bool kMasked, int kPoly>
 SA_DEV float s_row_exp_pack(uint32_t (&r)[128], float scale_log2, float neg_m, int lim) {
   float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};

@@ -266,13 +266,16 @@ fwd_pair_kernel(const __grid_constant__ PairParams p) {
         const float neg_m = (m_new == -INFINITY) ? 0.f : -m_new;
         l += masked ? s_row_exp_pack<true, SA_FWD_POLY>(r, p.scale_log2, neg_m, lim)
                     : s_row_exp_pack<false, SA_FWD_POLY>(r, p.scale_log2, neg_m, lim);
+        if (trace_lane) SA_TR(grp ? 14 : 10);
+        SA_TMEM_ST32(t_s + 0, (r + 0));
+        SA_TMEM_ST32(t_s + 32, (r + 32));
       } else {
+        uint32_t z[32];  // tile above this CTA's diagonal: P = 0
 #pragma unroll
-        for (int i = 0; i < 64; i++) r[i] = 0u;  // tile above this CTA's diagonal: P = 0
+        for (int i = 0; i < 32; i++) z[i] = 0u;
+        SA_TMEM_ST32(t_s + 0, z);
+        SA_TMEM_ST32(t_s + 32, z);
       }
-      if (trace_lane) SA_TR(grp ? 14 : 10);
-      SA_TMEM_ST32(t_s + 0, (r + 0));
-      SA_TMEM_ST32(t_s + 32, (r + 32));
       if (__any_sync(0xffffffffu, resc)) {
         // O holds PV(0..j-1) relative to m_prev: rescale once PV(j-1) has landed
         mbar_wait(&bar.pv_done[(j - 1) % kSt], ((j - 1) / kSt) & 1);
