@@ -61,8 +61,23 @@ SA_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
                ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// try_wait suspends the warp (it wakes when the phase completes) for up to a time limit;
+// without a hint that limit is short and a waiting warp spins every few tens of cycles,
+// taking issue slots from the compute warps on its SM sub-partition.  The hint is in ns.
+#ifndef SA_MBAR_SUSPEND_NS
+#define SA_MBAR_SUSPEND_NS 0x989680
+#endif
 SA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
+#if SA_MBAR_SUSPEND_NS
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.b32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "n"(SA_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
       "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P, [%1], %2;\n\t"
@@ -70,7 +85,13 @@ SA_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
+}
+SA_DEV uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 // Non-blocking probe of a phase (for issuers that poll several barriers).
 SA_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
@@ -84,11 +105,13 @@ SA_DEV bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU.
+// Bounded wait: a pipeline bug traps (launch error) instead of hanging the GPU -- after
+// 4 s of waiting on one phase (every legitimate wait here is microseconds).
 SA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t spins = 0;
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(bar, parity)) {
-    if (++spins > (1u << 25)) __trap();
+    if (globaltimer_ns() - t0 > 4000000000ull) __trap();
   }
 }
 
