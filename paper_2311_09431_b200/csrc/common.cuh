@@ -11,6 +11,7 @@
 //     LBO = panel stride (next 64 MN elements), SBO = 1024 (next 8 K rows).
 #pragma once
 #include <cstdint>
+#include "../../include/striped_attn.h"  // SA_MASK_* (the softmax helpers)
 #include <cuda_bf16.h>
 #include <cuda.h>
 
