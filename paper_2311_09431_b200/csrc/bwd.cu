@@ -566,9 +566,11 @@ __global__ void __launch_bounds__(512, 1) bwd_kernel(const __grid_constant__ Bwd
         // CTAs of lower j have lower blockIdx (scheduled earlier), so the wait cannot
         // deadlock; the semaphore counts this launch's contributions to tile i.
         const int want = j - p.j_begin;
-        uint32_t spins = 0;
-        while (ld_acquire_gpu(sem) != want)
-          if (++spins > (1u << 30)) __trap();
+        if (ld_acquire_gpu(sem) != want) {
+          const uint64_t t0 = globaltimer_ns();  // bounded: trap after 4 s (as mbar_wait)
+          while (ld_acquire_gpu(sem) != want)
+            if (globaltimer_ns() - t0 > 4000000000ull) __trap();
+        }
         fence_proxy_async_global();  // the previous adder's TMA writes before ours
       }
       __syncwarp();  // reconverge warp 12 before the named barriers below
