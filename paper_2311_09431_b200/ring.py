@@ -22,7 +22,8 @@ The hop itself is pluggable (``Comm``):
 
 Backward (no reference counterpart): fp32 dK/dV accumulators ride with their K/V
 stripe and arrive home after N hops; dQ accumulates locally.  Each round runs in three
-key parts (``kv_parts``) and each part's dK/dV rows leave as soon as that part retires.
+key parts (``kv_parts``: upper half, lower half) and each part's dK/dV rows leave as soon
+as that part retires.
 
 Block ops are pluggable (``BlockOps``): the default is the CUDA library (``ops.py``);
 CPU tests inject an oracle-backed implementation to test this host logic over ``gloo``
@@ -395,15 +396,17 @@ class _HopTimer:
 
 def kv_parts(c: int, tile: int = 128) -> list:
     """Row ranges of the held stripe's keys, in launch order, for the backward's
-    pipelined dK/dV hop: the upper half first (cheapest per row under a causal mask), then
-    the next quarter, the lowest quarter last, so the exposed hop is a quarter of the rows.
-    Blocks of fewer than 4 key tiles run in one part."""
+    pipelined dK/dV hop: the upper half first (a quarter of the work under a causal mask),
+    then the lower half.  Round i+1 launches its parts in the same order, so each part's
+    accumulator rows have the previous parts' compute time to arrive: no hop is exposed.
+    Two parts cost 1.0 % of the block at c = 32k (3 parts -- upper half, next quarter,
+    lowest quarter -- cost 2.8 %, `scripts/parts_probe.py`).  Blocks of fewer than 2 key
+    tiles run in one part."""
     nt = -(-c // tile)
-    if nt < 4:
+    if nt < 2:
         return [(0, c)]
-    b1, b2 = nt // 4, nt // 2
-    rows = lambda t: min(c, t * tile)
-    return [(rows(b2), c), (rows(b1), rows(b2)), (0, rows(b1))]
+    mid = min(c, (nt // 2) * tile)
+    return [(mid, c), (0, mid)]
 
 
 class Workspace:

@@ -175,12 +175,15 @@ def test_key_range_parts_equal_whole_block(ops, kind):
     acc = lambda h: torch.zeros(c, h, d, device="cuda")
     full = [acc(hq), acc(hkv), acc(hkv)]
     ops.bwd_block(q, k, v, do, lse, dsum, *full, 0.09, kind)
-    parts = [acc(hq), acc(hkv), acc(hkv)]
-    assert len(kv_parts(c)) == 3
-    for r0, r1 in kv_parts(c):
-        ops.bwd_block(q, k, v, do, lse, dsum, *parts, 0.09, kind, key_rows=(r0, r1))
-    torch.cuda.synchronize()
-    assert torch.equal(full[1], parts[1]) and torch.equal(full[2], parts[2])
-    assert (full[0] - parts[0]).abs().max().item() <= 1e-4 * max(1.0, full[0].abs().max().item())
+    assert len(kv_parts(c)) == 2
+    # the ring's two parts, and a three-part split (any tile-aligned ranges)
+    for ranges in (kv_parts(c), [(512, c), (256, 512), (0, 256)]):
+        parts = [acc(hq), acc(hkv), acc(hkv)]
+        for r0, r1 in ranges:
+            ops.bwd_block(q, k, v, do, lse, dsum, *parts, 0.09, kind, key_rows=(r0, r1))
+        torch.cuda.synchronize()
+        assert torch.equal(full[1], parts[1]) and torch.equal(full[2], parts[2])
+        assert (full[0] - parts[0]).abs().max().item() <= \
+            1e-4 * max(1.0, full[0].abs().max().item())
     with pytest.raises(Exception):
         ops.bwd_block(q, k, v, do, lse, dsum, *parts, 0.09, kind, key_rows=(100, 300))

@@ -2,7 +2,7 @@
 
 * configs[0] exactly: S = 8192, 8 heads, d 64, N = 4 ranks, striped AND ring, forward and
   backward, run by the real ring driver (ring_forward / ring_backward with its side
-  streams, double buffers and 3-part dK/dV hops) with the 4 ranks as threads sharing
+  streams, double buffers and 2-part dK/dV hops) with the 4 ranks as threads sharing
   this GPU (ring.LocalComm: copy-engine hops) -- against the fp64 dense oracle
   (oracle/ringref.py: dense_forward pinned to the reference's simulate, dense_backward
   pinned by autograd / finite differences).

@@ -5,7 +5,7 @@ The forward and dK / dV are deterministic by construction (one CTA owns each out
 the ring's travelling accumulators add once per round in round order).  dQ is
 reduce-added by many key-tile CTAs; with ``deterministic=True`` the adds into each query
 tile are ordered by key tile (sa_bwd_block_ex's dq_semaphore), so reruns -- on one GPU,
-and through the threaded ring with its 3-part launches -- are bit-identical."""
+and through the threaded ring with its 2-part launches -- are bit-identical."""
 
 import math
 

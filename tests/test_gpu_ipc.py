@@ -2,7 +2,7 @@
 
 World sizes 2 and 4 as processes sharing cuda:0 (gloo only for the rendezvous / store):
 the unchanged ring_forward / ring_backward with real kernels, side streams, double
-buffers and the 3-part dK/dV hops, every hop a cudaMemcpyAsync into the next process's
+buffers and the 2-part dK/dV hops, every hop a cudaMemcpyAsync into the next process's
 IPC-mapped receive buffer ordered by interprocess events -- against the fp64 oracle.
 No kernel waits on another process (the waits are stream-level event waits), so the
 ranks need not run concurrently."""

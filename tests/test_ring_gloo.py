@@ -75,7 +75,7 @@ def _worker(rank, world, port, layout, result_q, c_rank=16):
 @pytest.mark.parametrize("world,c_rank", [(2, 16), (4, 16), (2, 512)])
 @pytest.mark.parametrize("layout", ["striped", "ring"])
 def test_ring_driver_over_gloo(world, c_rank, layout):
-    """c_rank 512: the backward runs each block in 3 key parts whose dK/dV rows hop
+    """c_rank 512: the backward runs each block in 2 key parts whose dK/dV rows hop
     separately (ring.kv_parts)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
